@@ -1,0 +1,190 @@
+/*
+ * otf_b200.h — C ABI of the B200 (sm_100a) on-the-fly retrieval hot path.
+ *
+ * This is the drop-in boundary for the reference's scoring / ranking / Pegasos path
+ * (arXiv 1407.4764 reference package, /root/reference/pkg/src/otf_retrieval). The reference
+ * is pure Python + numpy; its "FFI" for this path is the set of Python functions listed next
+ * to each entry point below. The Python host package (paper_1407_4764_b200) binds these
+ * symbols with ctypes and keeps the reference's names, argument meaning and error types.
+ *
+ * Conventions
+ *   - Every entry point returns an int status (OTF_OK == 0). On failure, otf_last_error()
+ *     returns a thread-local, NUL-terminated message describing the last error of the
+ *     calling thread. Status codes map 1:1 onto the reference's exception hierarchy
+ *     (errors.py:10-51): see OTF_ERR_*.
+ *   - `mem` arguments say where caller pointers live: OTF_MEM_HOST (pageable or pinned host
+ *     memory; the call is synchronous and copies in/out) or OTF_MEM_DEVICE (device pointers on
+ *     the handle's device; the call is asynchronous on `stream`, a cudaStream_t passed as
+ *     void*, NULL = the handle's own stream).
+ *   - Scores are computed with the semantics of the reference: dense/binary scores are
+ *     float32 of <x, float32(w)> (ranker.py:69, :89-93), PQ scores are float64 of the
+ *     float64 LUT sum (pq.py:248-276). Ranked lists order by (-score, id) with ties toward
+ *     the smallest id (ranker.py:97-143) and report scores as float64.
+ *   - No torch types, no C++ types: plain pointers and sizes only.
+ */
+#ifndef OTF_B200_H
+#define OTF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference exception it maps to) ---------------------------------- */
+#define OTF_OK 0
+#define OTF_ERR_CONFIG 1       /* ConfigError            errors.py:30 */
+#define OTF_ERR_NOT_READY 2    /* NotReadyError          errors.py:38 */
+#define OTF_ERR_INSUFFICIENT 3 /* InsufficientDataError  errors.py:34 */
+#define OTF_ERR_CORRUPTION 4   /* CorruptionError        errors.py:18 */
+#define OTF_ERR_EMPTY 5        /* EmptyStoreError        errors.py:22 */
+#define OTF_ERR_CUDA 6         /* RetrievalError         errors.py:10 (CUDA failure) */
+#define OTF_ERR_NCCL 7         /* RetrievalError         errors.py:10 (collective)   */
+
+#define OTF_MEM_HOST 0
+#define OTF_MEM_DEVICE 1
+
+#define OTF_KIND_DENSE 0
+#define OTF_KIND_PQ 1
+#define OTF_KIND_BINARY 2
+
+#define OTF_F32 0
+#define OTF_F64 1
+
+/* ---- library ------------------------------------------------------------------------- */
+const char* otf_last_error(void);
+int otf_abi_version(void);
+int otf_device_count(int* out);
+/* Names of the kernels this build contains, ';'-separated (for launch accounting). */
+const char* otf_kernel_names(void);
+/* Number of kernel launches issued by this process since load (all devices). */
+int64_t otf_launch_count(void);
+
+/* ---- repositories: ranker.py:146-281 (Repository) ------------------------------------ */
+typedef struct otf_repo otf_repo;
+
+/* Repository.dense(store) — ranker.py:176-178. data is (n, dim) float32 row-major.
+ * ids: n int64 (NULL = id_base + row). If mem == OTF_MEM_DEVICE and borrow != 0 the handle
+ * reads `data` in place (caller keeps it alive); otherwise it copies into its own HBM. */
+int otf_repo_create_dense(int device, const float* data, int64_t n, int32_t dim,
+                          const int64_t* ids, int64_t id_base, int mem, int borrow,
+                          otf_repo** out);
+
+/* Repository.quantized(codebook, codes, ids, names) — ranker.py:180-192.
+ * codes (n, num_blocks) uint8; centroids (num_blocks, num_centroids, subdim) float32 host. */
+int otf_repo_create_pq(int device, const uint8_t* codes, int64_t n, const float* centroids,
+                       int32_t num_blocks, int32_t num_centroids, int32_t subdim,
+                       const int64_t* ids, int64_t id_base, int mem, int borrow,
+                       otf_repo** out);
+
+/* Repository.binary(codec, codes, ids, names) — ranker.py:194-209.
+ * codes (n, ceil(output_bits/8)) uint8, LSB-first bit order (binary.py:106,119). */
+int otf_repo_create_binary(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
+                           const int64_t* ids, int64_t id_base, int mem, int borrow,
+                           otf_repo** out);
+
+/* Repository.without_ids(excluded) — ranker.py:254-270: new handle holding rows `rows`
+ * (host int64 row positions, ascending) of `src`, ids preserved, payload gathered on device. */
+int otf_repo_subset(const otf_repo* src, const int64_t* rows, int64_t n_keep, otf_repo** out);
+
+int otf_repo_destroy(otf_repo* repo);
+
+/* count / model_dim / payload_bytes / kind — ranker.py:213-231. */
+int otf_repo_info(const otf_repo* repo, int32_t* kind, int64_t* count, int32_t* model_dim,
+                  int64_t* payload_bytes, int32_t* device);
+
+/* Repository.score(model) — ranker.py:233-240. w: model_dim float64.
+ * out: count float32 (dense, binary) or float64 (pq). */
+int otf_repo_score(otf_repo* repo, const double* w, void* out, int mem, void* stream);
+
+/* Repository.rank(model, k) — ranker.py:272-281 (score + top_k, ranker.py:97-143).
+ * Writes n_out = min(max(k,0), count) entries: ids (int64), scores (float64), and
+ * optionally rows (int64 row positions, for names; may be NULL). If out_n is non-NULL it
+ * receives n_out. With mem == OTF_MEM_DEVICE everything is asynchronous on `stream`. */
+int otf_repo_rank(otf_repo* repo, const double* w, int64_t k, int64_t* out_ids,
+                  double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
+                  void* stream);
+
+/* Capture repo's rank(k) for a device-resident w into a CUDA graph and replay it
+ * (the live ranker re-ranks every tau with a new w in the same buffer). Device memory only. */
+int otf_repo_rank_graph(otf_repo* repo, const double* w_dev, int64_t k, int64_t* ids_dev,
+                        double* scores_dev, int64_t* rows_dev, void* stream);
+
+/* ---- stateless primitives (module functions) ------------------------------------------ */
+/* score_dense(model, X) — ranker.py:63-69 */
+int otf_score_dense(int device, const float* X, int64_t n, int32_t dim, const double* w,
+                    float* out, int mem, void* stream);
+/* build_score_lut(w, codebook) — pq.py:248-259: lut (M, K) float64 in numpy einsum order. */
+int otf_pq_build_lut(int device, const float* centroids, int32_t num_blocks,
+                     int32_t num_centroids, int32_t subdim, const double* w, double* lut,
+                     int mem, void* stream);
+/* score_codes(lut, codes) — pq.py:262-276: float64 numpy pairwise sum over blocks.
+ * A code >= num_centroids is reported as OTF_ERR_CORRUPTION (the reference raises a numpy
+ * IndexError only when the code is >= the LUT width; documented deviation). */
+int otf_pq_score_codes(int device, const double* lut, int32_t num_blocks,
+                       int32_t num_centroids, const uint8_t* codes, int64_t n, double* out,
+                       int mem, void* stream);
+/* score_binary(model, codes, output_bits) — ranker.py:78-94 */
+int otf_score_binary(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
+                     const double* w, float* out, int mem, void* stream);
+/* unpack_bits(codes, output_bits) — binary.py:110-120: (n, output_bits) float32 {0,1}. */
+int otf_unpack_bits(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
+                    float* out, int mem, void* stream);
+/* binarize(codec, X) — binary.py:86-107: frame (output_bits, input_dim) float64 row-major,
+ * centering (input_dim) float32, X (n, input_dim) float64 -> (n, ceil(output_bits/8)) u8. */
+int otf_binarize(int device, const double* frame, const float* centering, int32_t input_dim,
+                 int32_t output_bits, const double* X, int64_t n, uint8_t* out, int mem,
+                 void* stream);
+/* hamming_distance(a, b) — binary.py:123-128 (row-wise, equal widths). */
+int otf_hamming(int device, const uint8_t* a, const uint8_t* b, int64_t n, int32_t width,
+                int64_t* out, int mem, void* stream);
+/* top_k(scores, k, ids) — ranker.py:97-143. scores float32 (dtype OTF_F32) or float64;
+ * ids n int64 or NULL (0..n-1). Output as otf_repo_rank. */
+int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const int64_t* ids,
+              int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+              int64_t* out_n, int mem, void* stream);
+
+/* ---- Pegasos trainer: trainer.py:51-173 ------------------------------------------------ */
+/* _apply_update + pegasos_step gather — trainer.py:51-71, :100-106. Device pointers only.
+ * w (d) float64 updated in place; pos (n_pos, d), neg (n_neg, d) of dtype pos_dtype /
+ * neg_dtype (OTF_F32 | OTF_F64); pos_idx, neg_idx: `half` device int64 indices each.
+ * eta_lam_shrink = 1 - eta*lam and eta_over_b = eta / batch_size are computed by the caller
+ * exactly as the reference does in Python doubles; radius = 1/sqrt(lam) (project != 0). */
+int otf_pegasos_update(int device, double* w, int32_t d, const void* pos, int32_t pos_dtype,
+                       int64_t n_pos, const void* neg, int32_t neg_dtype, int64_t n_neg,
+                       const int64_t* pos_idx, const int64_t* neg_idx, int32_t half,
+                       double shrink, double eta_over_b, int project, double radius,
+                       void* stream);
+
+/* _apply_update on a host batch (trainer.py:51-71): batch (2*half, d) float64 host rows,
+ * positives first; w (d) float64 host, updated in place. Stateless pegasos_step primitive. */
+int otf_pegasos_step_host(int device, double* w, int32_t d, const double* batch, int32_t half,
+                          double shrink, double eta_over_b, int project, double radius);
+
+typedef struct otf_trainer otf_trainer;
+/* OnlineTrainer(dim, negatives, cfg) — trainer.py:109-143; negatives copied to HBM once. */
+int otf_trainer_create(int device, int32_t dim, const void* negatives, int32_t neg_dtype,
+                       int64_t n_neg, int mem, otf_trainer** out);
+int otf_trainer_destroy(otf_trainer* tr);
+/* Append positives to the trainer's device pool (session.py:62-93 PositivePool.append). */
+int otf_trainer_append_positives(otf_trainer* tr, const void* rows, int32_t dtype,
+                                 int64_t n_rows, int mem);
+int otf_trainer_pool_size(const otf_trainer* tr, int64_t* n_pos);
+/* One step (trainer.py:145-159) with host-sampled indices (numpy PCG64 stream, as the
+ * reference draws them). If `positives` is non-NULL the B/2 sampled rows are taken from
+ * that host array (any pool the caller holds); otherwise from the device pool. */
+int otf_trainer_step(otf_trainer* tr, const void* positives, int32_t pos_dtype, int64_t n_pos,
+                     const int64_t* pos_idx, const int64_t* neg_idx, int32_t half,
+                     double shrink, double eta_over_b, int project, double radius);
+/* Snapshot copy of w (trainer.py:161-173): host float64 (mem HOST) or device. */
+int otf_trainer_weights(otf_trainer* tr, double* out, int mem);
+int otf_trainer_set_weights(otf_trainer* tr, const double* w, int mem);
+/* Device pointer of w (float64, dim) for zero-copy ranking on the same device. */
+int otf_trainer_weights_ptr(otf_trainer* tr, const double** out);
+/* The trainer's CUDA stream (high priority; runs concurrently with ranking). */
+int otf_trainer_stream(otf_trainer* tr, void** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OTF_B200_H */

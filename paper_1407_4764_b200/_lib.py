@@ -1,0 +1,150 @@
+"""ctypes binding of ``libotf_b200.so`` (the C ABI in include/otf_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is visible, every entry
+point raises ``RetrievalError`` — the product path is the sm_100a kernels or nothing.
+ctypes releases the GIL for the duration of each foreign call, so the ranker and trainer
+threads of a live session (session.py:295-359 in the reference) overlap on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import (
+    ConfigError,
+    CorruptionError,
+    EmptyStoreError,
+    InsufficientDataError,
+    NotReadyError,
+    RetrievalError,
+)
+
+LIB_PATH = Path(__file__).resolve().parent / "libotf_b200.so"
+
+OK = 0
+MEM_HOST, MEM_DEVICE = 0, 1
+KIND_DENSE, KIND_PQ, KIND_BINARY = 0, 1, 2
+F32, F64 = 0, 1
+
+_ERRORS = {
+    1: ConfigError,
+    2: NotReadyError,
+    3: InsufficientDataError,
+    4: CorruptionError,
+    5: EmptyStoreError,
+    6: RetrievalError,
+    7: RetrievalError,
+}
+
+_vp, _i64, _i32, _int, _dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_int, C.c_double
+_P = C.POINTER
+
+# name -> argtypes (all return int unless listed in _RESTYPE)
+SIGNATURES: dict[str, list] = {
+    "otf_last_error": [],
+    "otf_abi_version": [],
+    "otf_device_count": [_P(_int)],
+    "otf_kernel_names": [],
+    "otf_launch_count": [],
+    "otf_repo_create_dense": [_int, _vp, _i64, _i32, _vp, _i64, _int, _int, _P(_vp)],
+    "otf_repo_create_pq": [_int, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _int, _int, _P(_vp)],
+    "otf_repo_create_binary": [_int, _vp, _i64, _i32, _vp, _i64, _int, _int, _P(_vp)],
+    "otf_repo_subset": [_vp, _vp, _i64, _P(_vp)],
+    "otf_repo_destroy": [_vp],
+    "otf_repo_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64), _P(_i32)],
+    "otf_repo_score": [_vp, _vp, _vp, _int, _vp],
+    "otf_repo_rank": [_vp, _vp, _i64, _vp, _vp, _vp, _P(_i64), _int, _vp],
+    "otf_repo_rank_graph": [_vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "otf_score_dense": [_int, _vp, _i64, _i32, _vp, _vp, _int, _vp],
+    "otf_pq_build_lut": [_int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp],
+    "otf_pq_score_codes": [_int, _vp, _i32, _i32, _vp, _i64, _vp, _int, _vp],
+    "otf_score_binary": [_int, _vp, _i64, _i32, _vp, _vp, _int, _vp],
+    "otf_unpack_bits": [_int, _vp, _i64, _i32, _vp, _int, _vp],
+    "otf_binarize": [_int, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _int, _vp],
+    "otf_hamming": [_int, _vp, _vp, _i64, _i32, _vp, _int, _vp],
+    "otf_top_k": [_int, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp, _P(_i64), _int, _vp],
+    "otf_pegasos_update": [_int, _vp, _i32, _vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32,
+                           _dbl, _dbl, _int, _dbl, _vp],
+    "otf_pegasos_step_host": [_int, _vp, _i32, _vp, _i32, _dbl, _dbl, _int, _dbl],
+    "otf_trainer_create": [_int, _i32, _vp, _i32, _i64, _int, _P(_vp)],
+    "otf_trainer_destroy": [_vp],
+    "otf_trainer_append_positives": [_vp, _vp, _i32, _i64, _int],
+    "otf_trainer_pool_size": [_vp, _P(_i64)],
+    "otf_trainer_step": [_vp, _vp, _i32, _i64, _vp, _vp, _i32, _dbl, _dbl, _int, _dbl],
+    "otf_trainer_weights": [_vp, _vp, _int],
+    "otf_trainer_set_weights": [_vp, _vp, _int],
+    "otf_trainer_weights_ptr": [_vp, _P(_vp)],
+    "otf_trainer_stream": [_vp, _P(_vp)],
+}
+_RESTYPE = {"otf_last_error": C.c_char_p, "otf_kernel_names": C.c_char_p, "otf_launch_count": _i64}
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+_checked_device = False
+
+
+def load(require_device: bool = True) -> C.CDLL:
+    """Load the shared library (and, by default, insist on a visible CUDA device)."""
+    global _lib, _checked_device
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RetrievalError(
+                    f"{LIB_PATH.name} is not built; run paper_1407_4764_b200/_build.py "
+                    "(no CPU fallback exists)"
+                )
+            lib = C.CDLL(str(LIB_PATH))
+            for name, args in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPE.get(name, _int)
+            _lib = lib
+        if require_device and not _checked_device:
+            n = _int(0)
+            rc = _lib.otf_device_count(C.byref(n))
+            if rc != OK or n.value < 1:
+                raise RetrievalError("no CUDA device visible: the B200 retrieval path has no CPU fallback")
+            _checked_device = True
+        return _lib
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        lib = load(require_device=False)
+        msg = lib.otf_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RetrievalError)(msg)
+
+
+def ptr(a: np.ndarray | None) -> C.c_void_p | None:
+    if a is None:
+        return None
+    return C.c_void_p(a.ctypes.data)
+
+
+def tptr(t) -> C.c_void_p:
+    """Device pointer of a torch tensor."""
+    return C.c_void_p(t.data_ptr())
+
+
+_device = None
+
+
+def default_device() -> int:
+    global _device
+    if _device is None:
+        _device = int(os.environ.get("OTF_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    return _device
+
+
+def set_device(index: int) -> None:
+    global _device
+    _device = int(index)
+
+
+def launch_count() -> int:
+    return int(load(require_device=False).otf_launch_count())

@@ -1,0 +1,886 @@
+// otf_capi.cu — the extern "C" boundary (include/otf_b200.h): handles, memory ownership,
+// host<->device staging, error mapping. All compute is in the kernels of the other units.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "otf_b200.h"
+#include "otf_common.cuh"
+#include "otf_internal.h"
+
+namespace otf {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return OTF_ERR_CUDA;
+}
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  int d = device & 63;
+  if (cache[d] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[d] = v > 0 ? v : 1;
+  }
+  return cache[d];
+}
+
+// RAII device selection
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Simple device/pinned buffers ---------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes && p) return OTF_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) return OTF_OK;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    bytes = b;
+    return OTF_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes && p) return OTF_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) return OTF_OK;
+    cudaError_t e = cudaMallocHost(&p, b);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+    bytes = b;
+    return OTF_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace otf
+
+using namespace otf;
+
+struct otf_repo {
+  int device = 0;
+  int kind = OTF_KIND_DENSE;
+  int64_t n = 0;
+  int32_t model_dim = 0;   // d (dense), M*Q (pq), n_bits (binary)
+  int32_t M = 0, K = 0, Q = 0;
+  int64_t row_bytes = 0;
+  const void* payload = nullptr;  // device
+  bool owns_payload = false;
+  int64_t* ids = nullptr;          // device, nullable
+  int64_t id_base = 0;
+  float* cents = nullptr;          // pq centroids (device)
+  cudaStream_t stream = nullptr;
+  std::mutex mu;                   // one call at a time per handle
+  DevBuf w, w32, lut, scores, outbuf;
+  HostBuf h_w, h_out;
+  TopkWs topk;
+  // graph cache for otf_repo_rank_graph
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t g_k = -1;
+};
+
+struct otf_trainer {
+  int device = 0;
+  int32_t dim = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf w, neg, pos_pool, pos_stage, idx;
+  HostBuf h_stage, h_idx;
+  int neg_dtype = OTF_F32;
+  int64_t n_neg = 0;
+  int64_t n_pos = 0, pos_cap = 0;
+};
+
+namespace {
+
+cudaStream_t pick_stream(cudaStream_t own, void* user) {
+  return user ? static_cast<cudaStream_t>(user) : own;
+}
+
+int make_stream(cudaStream_t* s, bool high_priority) {
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  OTF_CUDA(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, high_priority ? hi : lo));
+  return OTF_OK;
+}
+
+int copy_in(void* dst, const void* src, size_t bytes, int mem, cudaStream_t st) {
+  if (bytes == 0) return OTF_OK;
+  OTF_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                           mem == OTF_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           st));
+  return OTF_OK;
+}
+
+int check_ids(const int64_t* ids, int64_t n, int mem) {
+  if (!ids || mem != OTF_MEM_HOST) return OTF_OK;
+  for (int64_t i = 0; i < n; ++i)
+    if (ids[i] < 0) return fail(OTF_ERR_CONFIG, "ids must be non-negative");
+  return OTF_OK;
+}
+
+int repo_common(otf_repo* r, int device, int64_t n, const int64_t* ids, int64_t id_base,
+                int mem) {
+  r->device = device;
+  r->n = n;
+  r->id_base = id_base;
+  int rc = make_stream(&r->stream, false);
+  if (rc) return rc;
+  if (ids) {
+    rc = check_ids(ids, n, mem);
+    if (rc) return rc;
+    OTF_CUDA(cudaMalloc(&r->ids, (size_t)(n > 0 ? n : 1) * sizeof(int64_t)));
+    rc = copy_in(r->ids, ids, (size_t)n * sizeof(int64_t), mem, r->stream);
+    if (rc) return rc;
+  }
+  return OTF_OK;
+}
+
+int take_payload(otf_repo* r, const void* data, size_t bytes, int mem, int borrow) {
+  if (mem == OTF_MEM_DEVICE && borrow) {
+    r->payload = data;
+    r->owns_payload = false;
+    return OTF_OK;
+  }
+  void* p = nullptr;
+  OTF_CUDA(cudaMalloc(&p, bytes > 0 ? bytes : 16));
+  r->payload = p;
+  r->owns_payload = true;
+  return copy_in(p, data, bytes, mem, r->stream);
+}
+
+void repo_free(otf_repo* r) {
+  if (!r) return;
+  DeviceGuard g(r->device);
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  if (r->owns_payload && r->payload) cudaFree(const_cast<void*>(r->payload));
+  if (r->ids) cudaFree(r->ids);
+  if (r->cents) cudaFree(r->cents);
+  r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->outbuf.release();
+  r->h_w.release(); r->h_out.release();
+  topk_ws_free(&r->topk);
+  if (r->stream) cudaStreamDestroy(r->stream);
+  delete r;
+}
+
+// Uploads w (host or device) into r->w; returns device pointer.
+int stage_w(otf_repo* r, const double* w, int mem, cudaStream_t st, const double** dw) {
+  const size_t bytes = (size_t)r->model_dim * sizeof(double);
+  if (mem == OTF_MEM_DEVICE) {
+    *dw = w;
+    return OTF_OK;
+  }
+  int rc = r->w.ensure(bytes);
+  if (rc) return rc;
+  rc = r->h_w.ensure(bytes);
+  if (rc) return rc;
+  std::memcpy(r->h_w.p, w, bytes);
+  OTF_CUDA(cudaMemcpyAsync(r->w.p, r->h_w.p, bytes, cudaMemcpyHostToDevice, st));
+  *dw = static_cast<const double*>(r->w.p);
+  return OTF_OK;
+}
+
+// Scores every row of r into `out` (device); returns dtype of the scores.
+int score_into(otf_repo* r, const double* dw, void* out, cudaStream_t st) {
+  int rc = OTF_OK;
+  if (r->kind == OTF_KIND_DENSE) {
+    if ((rc = r->w32.ensure((size_t)r->model_dim * sizeof(float)))) return rc;
+    if ((rc = launch_cast_w(dw, static_cast<float*>(r->w32.p), r->model_dim, st))) return rc;
+    return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim,
+                              static_cast<const float*>(r->w32.p), static_cast<float*>(out),
+                              r->device, st);
+  }
+  if (r->kind == OTF_KIND_PQ) {
+    if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
+    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
+      return rc;
+    return launch_pq_scan(static_cast<const uint8_t*>(r->payload), r->n, r->M,
+                          static_cast<const double*>(r->lut.p), r->K, static_cast<double*>(out),
+                          r->device, st);
+  }
+  // binary
+  const size_t lb = bin_lut_bytes(r->model_dim);
+  if (lb > 0) {
+    if ((rc = r->lut.ensure(lb))) return rc;
+    if ((rc = launch_bin_lut(dw, r->model_dim, static_cast<double*>(r->lut.p), st))) return rc;
+    return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim,
+                            static_cast<const double*>(r->lut.p), nullptr,
+                            static_cast<float*>(out), r->device, st);
+  }
+  if ((rc = r->w32.ensure((size_t)r->model_dim * sizeof(float)))) return rc;
+  if ((rc = launch_cast_w(dw, static_cast<float*>(r->w32.p), r->model_dim, st))) return rc;
+  return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, nullptr,
+                          static_cast<const float*>(r->w32.p), static_cast<float*>(out),
+                          r->device, st);
+}
+
+int score_dtype(const otf_repo* r) { return r->kind == OTF_KIND_PQ ? OTF_F64 : OTF_F32; }
+
+int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, double* scores,
+                int64_t* rows, cudaStream_t st) {
+  const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+  int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
+  if (rc) return rc;
+  if ((rc = score_into(r, dw, r->scores.p, st))) return rc;
+  return launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, ids,
+                     scores, rows, r->device, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* otf_last_error(void) { return g_last_error.c_str(); }
+int otf_abi_version(void) { return 1; }
+int64_t otf_launch_count(void) { return g_launches.load(); }
+
+const char* otf_kernel_names(void) {
+  return "dense_score_fast;dense_score_generic;cast_w_f32;pq_build_lut_kernel;pq_scan_fast;"
+         "pq_scan_generic;pq_check_codes;bin_build_nibble_lut;bin_score_fast;bin_score_generic;"
+         "bin_unpack;bin_binarize;bin_hamming;topk_coop_kernel;pegasos_kernel;gather_rows_kernel;"
+         "gather_i64_kernel";
+}
+
+int otf_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = n;
+  return OTF_OK;
+}
+
+int otf_repo_create_dense(int device, const float* data, int64_t n, int32_t dim,
+                          const int64_t* ids, int64_t id_base, int mem, int borrow,
+                          otf_repo** out) {
+  *out = nullptr;
+  if (dim <= 0 || n < 0) return fail(OTF_ERR_CONFIG, "dense repository needs dim > 0 and n >= 0");
+  DeviceGuard g(device);
+  otf_repo* r = new otf_repo();
+  r->kind = OTF_KIND_DENSE;
+  r->model_dim = dim;
+  r->row_bytes = (int64_t)dim * 4;
+  int rc = repo_common(r, device, n, ids, id_base, mem);
+  if (!rc) rc = take_payload(r, data, (size_t)n * dim * sizeof(float), mem, borrow);
+  if (!rc && cudaStreamSynchronize(r->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "create_dense");
+  if (rc) { repo_free(r); return rc; }
+  *out = r;
+  return OTF_OK;
+}
+
+int otf_repo_create_pq(int device, const uint8_t* codes, int64_t n, const float* centroids,
+                       int32_t num_blocks, int32_t num_centroids, int32_t subdim,
+                       const int64_t* ids, int64_t id_base, int mem, int borrow,
+                       otf_repo** out) {
+  *out = nullptr;
+  if (num_blocks <= 0 || subdim <= 0 || num_centroids <= 0 || num_centroids > 256 || n < 0)
+    return fail(OTF_ERR_CONFIG, "pq repository needs blocks, subdim > 0 and 1 <= centroids <= 256");
+  DeviceGuard g(device);
+  otf_repo* r = new otf_repo();
+  r->kind = OTF_KIND_PQ;
+  r->M = num_blocks; r->K = num_centroids; r->Q = subdim;
+  r->model_dim = num_blocks * subdim;
+  r->row_bytes = num_blocks;
+  int rc = repo_common(r, device, n, ids, id_base, mem);
+  if (!rc) rc = take_payload(r, codes, (size_t)n * num_blocks, mem, borrow);
+  const size_t cb = (size_t)num_blocks * num_centroids * subdim * sizeof(float);
+  if (!rc && cudaMalloc(&r->cents, cb) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "cudaMalloc centroids");
+  if (!rc) rc = copy_in(r->cents, centroids, cb, OTF_MEM_HOST, r->stream);
+  // codes must index the codebook (pq.py:240-241 / load_pq_codes :326-329)
+  unsigned int* bad = nullptr;
+  if (!rc && num_centroids < 256) {
+    if (cudaMalloc(&bad, sizeof(unsigned int)) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "cudaMalloc");
+    if (!rc) { cudaMemsetAsync(bad, 0, sizeof(unsigned int), r->stream);
+      rc = launch_pq_check(static_cast<const uint8_t*>(r->payload), n * num_blocks, num_centroids, bad, device, r->stream); }
+  }
+  if (!rc && cudaStreamSynchronize(r->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "create_pq");
+  if (!rc && bad) {
+    unsigned int hb = 0;
+    cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+    if (hb) rc = fail(OTF_ERR_CORRUPTION, "code value out of range for " + std::to_string(num_centroids) + " centroids");
+  }
+  if (bad) cudaFree(bad);
+  if (rc) { repo_free(r); return rc; }
+  *out = r;
+  return OTF_OK;
+}
+
+int otf_repo_create_binary(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
+                           const int64_t* ids, int64_t id_base, int mem, int borrow,
+                           otf_repo** out) {
+  *out = nullptr;
+  if (output_bits <= 0 || n < 0) return fail(OTF_ERR_CONFIG, "binary repository needs output_bits > 0");
+  DeviceGuard g(device);
+  otf_repo* r = new otf_repo();
+  r->kind = OTF_KIND_BINARY;
+  r->model_dim = output_bits;
+  r->row_bytes = (output_bits + 7) / 8;
+  int rc = repo_common(r, device, n, ids, id_base, mem);
+  if (!rc) rc = take_payload(r, codes, (size_t)n * r->row_bytes, mem, borrow);
+  if (!rc && cudaStreamSynchronize(r->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "create_binary");
+  if (rc) { repo_free(r); return rc; }
+  *out = r;
+  return OTF_OK;
+}
+
+int otf_repo_subset(const otf_repo* src_c, const int64_t* rows, int64_t n_keep, otf_repo** out) {
+  *out = nullptr;
+  otf_repo* src = const_cast<otf_repo*>(src_c);
+  std::lock_guard<std::mutex> lk(src->mu);
+  DeviceGuard g(src->device);
+  for (int64_t i = 0; i < n_keep; ++i)
+    if (rows[i] < 0 || rows[i] >= src->n) return fail(OTF_ERR_CONFIG, "subset row out of range");
+  otf_repo* r = new otf_repo();
+  r->device = src->device; r->kind = src->kind; r->n = n_keep; r->model_dim = src->model_dim;
+  r->M = src->M; r->K = src->K; r->Q = src->Q; r->row_bytes = src->row_bytes;
+  r->id_base = 0;
+  int rc = make_stream(&r->stream, false);
+  DevBuf d_rows;
+  if (!rc) rc = d_rows.ensure((size_t)(n_keep > 0 ? n_keep : 1) * sizeof(int64_t));
+  if (!rc) rc = copy_in(d_rows.p, rows, (size_t)n_keep * sizeof(int64_t), OTF_MEM_HOST, r->stream);
+  void* p = nullptr;
+  if (!rc && cudaMalloc(&p, (size_t)(n_keep > 0 ? n_keep : 1) * r->row_bytes) != cudaSuccess)
+    rc = cuda_fail(cudaGetLastError(), "cudaMalloc subset");
+  if (!rc) { r->payload = p; r->owns_payload = true; }
+  if (!rc && cudaMalloc(&r->ids, (size_t)(n_keep > 0 ? n_keep : 1) * sizeof(int64_t)) != cudaSuccess)
+    rc = cuda_fail(cudaGetLastError(), "cudaMalloc subset ids");
+  // order the subset after any pending work on the source stream
+  if (!rc) { cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, src->stream); cudaStreamWaitEvent(r->stream, ev, 0); cudaEventDestroy(ev); }
+  if (!rc) rc = launch_gather_rows(static_cast<const uint8_t*>(src->payload), r->row_bytes,
+                                   static_cast<const int64_t*>(d_rows.p), n_keep,
+                                   static_cast<uint8_t*>(p), r->device, r->stream);
+  if (!rc) rc = launch_gather_i64(src->ids, static_cast<const int64_t*>(d_rows.p), n_keep,
+                                  src->id_base, r->ids, r->stream);
+  if (!rc && src->cents) {
+    const size_t cb = (size_t)src->M * src->K * src->Q * sizeof(float);
+    if (cudaMalloc(&r->cents, cb) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "cudaMalloc cents");
+    if (!rc) rc = copy_in(r->cents, src->cents, cb, OTF_MEM_DEVICE, r->stream);
+  }
+  if (!rc && cudaStreamSynchronize(r->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "subset");
+  d_rows.release();
+  if (rc) { repo_free(r); return rc; }
+  *out = r;
+  return OTF_OK;
+}
+
+int otf_repo_destroy(otf_repo* repo) {
+  repo_free(repo);
+  return OTF_OK;
+}
+
+int otf_repo_info(const otf_repo* r, int32_t* kind, int64_t* count, int32_t* model_dim,
+                  int64_t* payload_bytes, int32_t* device) {
+  if (kind) *kind = r->kind;
+  if (count) *count = r->n;
+  if (model_dim) *model_dim = r->model_dim;
+  if (payload_bytes) *payload_bytes = r->n * r->row_bytes;
+  if (device) *device = r->device;
+  return OTF_OK;
+}
+
+int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
+  const double* dw = nullptr;
+  int rc = stage_w(r, w, mem, st, &dw);
+  if (rc) return rc;
+  const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+  if (mem == OTF_MEM_DEVICE) return score_into(r, dw, out, st);
+  if ((rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es))) return rc;
+  if ((rc = score_into(r, dw, r->scores.p, st))) return rc;
+  OTF_CUDA(cudaMemcpyAsync(out, r->scores.p, (size_t)r->n * es, cudaMemcpyDeviceToHost, st));
+  OTF_CUDA(cudaStreamSynchronize(st));
+  return OTF_OK;
+}
+
+int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, double* out_scores,
+                  int64_t* out_rows, int64_t* out_n, int mem, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  if (out_n) *out_n = k_eff;
+  if (k_eff == 0) return OTF_OK;
+  cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
+  const double* dw = nullptr;
+  int rc = stage_w(r, w, mem, st, &dw);
+  if (rc) return rc;
+  if (mem == OTF_MEM_DEVICE) return rank_device(r, dw, k_eff, out_ids, out_scores, out_rows, st);
+  const size_t bytes = (size_t)k_eff * 24;
+  if ((rc = r->outbuf.ensure(bytes))) return rc;
+  if ((rc = r->h_out.ensure(bytes))) return rc;
+  int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
+  double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
+  if ((rc = rank_device(r, dw, k_eff, d_ids, d_sc, d_rows, st))) return rc;
+  OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
+  OTF_CUDA(cudaStreamSynchronize(st));
+  const int64_t* h_ids = static_cast<const int64_t*>(r->h_out.p);
+  std::memcpy(out_ids, h_ids, (size_t)k_eff * 8);
+  std::memcpy(out_scores, h_ids + k_eff, (size_t)k_eff * 8);
+  if (out_rows) std::memcpy(out_rows, h_ids + 2 * k_eff, (size_t)k_eff * 8);
+  return OTF_OK;
+}
+
+int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* ids_dev,
+                        double* scores_dev, int64_t* rows_dev, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  if (k_eff == 0) return OTF_OK;
+  cudaStream_t st = pick_stream(r->stream, stream);
+  const void* key[6] = {w_dev, ids_dev, scores_dev, rows_dev, stream, nullptr};
+  bool hit = r->gexec && r->g_k == k_eff;
+  for (int i = 0; i < 5 && hit; ++i) hit = key[i] == r->g_key[i];
+  if (!hit) {
+    if (r->gexec) { cudaGraphExecDestroy(r->gexec); r->gexec = nullptr; }
+    // allocate everything outside capture
+    const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+    int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
+    if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
+    if (!rc) rc = r->w32.ensure((size_t)r->model_dim * sizeof(float));
+    if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
+    if (!rc && (r->kind == OTF_KIND_BINARY) && bin_lut_bytes(r->model_dim))
+      rc = r->lut.ensure(bin_lut_bytes(r->model_dim));
+    if (rc) return rc;
+    cudaStream_t cap;
+    OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    OTF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    cudaStreamDestroy(cap);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { r->gexec = nullptr; return cuda_fail(e, "cudaGraphInstantiate"); }
+    for (int i = 0; i < 5; ++i) r->g_key[i] = key[i];
+    r->g_k = k_eff;
+  }
+  OTF_CUDA(cudaGraphLaunch(r->gexec, st));
+  count_launch(3);
+  return OTF_OK;
+}
+
+// ---- stateless primitives ----------------------------------------------------------------------
+namespace {
+struct Scratch {
+  std::vector<DevBuf> bufs;
+  cudaStream_t st = nullptr;
+  int device = 0;
+  ~Scratch() {
+    if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+    for (auto& b : bufs) b.release();
+  }
+  int init(int dev) {
+    device = dev;
+    OTF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    return OTF_OK;
+  }
+  // device copy of a host input (or pass-through for device memory)
+  int in(const void* src, size_t bytes, int mem, const void** dptr) {
+    if (mem == OTF_MEM_DEVICE) { *dptr = src; return OTF_OK; }
+    bufs.emplace_back();
+    int rc = bufs.back().ensure(bytes > 0 ? bytes : 16);
+    if (rc) return rc;
+    if (bytes) OTF_CUDA(cudaMemcpyAsync(bufs.back().p, src, bytes, cudaMemcpyHostToDevice, st));
+    *dptr = bufs.back().p;
+    return OTF_OK;
+  }
+  int outbuf(void* user, size_t bytes, int mem, void** dptr) {
+    if (mem == OTF_MEM_DEVICE) { *dptr = user; return OTF_OK; }
+    bufs.emplace_back();
+    int rc = bufs.back().ensure(bytes > 0 ? bytes : 16);
+    if (rc) return rc;
+    *dptr = bufs.back().p;
+    return OTF_OK;
+  }
+  int out(void* user, const void* dptr, size_t bytes, int mem) {
+    if (mem == OTF_MEM_DEVICE) return OTF_OK;
+    if (bytes) OTF_CUDA(cudaMemcpyAsync(user, dptr, bytes, cudaMemcpyDeviceToHost, st));
+    OTF_CUDA(cudaStreamSynchronize(st));
+    return OTF_OK;
+  }
+};
+}  // namespace
+
+#define STATELESS_BEGIN(device, mem, stream)                                    \
+  DeviceGuard _g(device);                                                       \
+  Scratch S;                                                                    \
+  cudaStream_t st;                                                              \
+  if (mem == OTF_MEM_DEVICE) { st = static_cast<cudaStream_t>(stream); S.device = device; } \
+  else { int _rc = S.init(device); if (_rc) return _rc; st = S.st; }              \
+  int rc = OTF_OK;
+
+int otf_score_dense(int device, const float* X, int64_t n, int32_t dim, const double* w, float* out,
+                    int mem, void* stream) {
+  if (dim <= 0) return fail(OTF_ERR_CONFIG, "dim must be positive");
+  STATELESS_BEGIN(device, mem, stream)
+  const void *dX, *dw; void* dout; DevBuf w32;
+  if ((rc = S.in(X, (size_t)n * dim * 4, mem, &dX))) return rc;
+  if ((rc = S.in(w, (size_t)dim * 8, mem, &dw))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * 4, mem, &dout))) return rc;
+  if ((rc = w32.ensure((size_t)dim * 4))) return rc;
+  if ((rc = launch_cast_w(static_cast<const double*>(dw), static_cast<float*>(w32.p), dim, st))) return rc;
+  if ((rc = launch_dense_score(static_cast<const float*>(dX), n, dim, static_cast<const float*>(w32.p),
+                               static_cast<float*>(dout), device, st))) return rc;
+  rc = S.out(out, dout, (size_t)n * 4, mem);
+  if (mem == OTF_MEM_DEVICE) cudaStreamSynchronize(st);  // w32 is freed on return
+  w32.release();
+  return rc;
+}
+
+int otf_pq_build_lut(int device, const float* centroids, int32_t M, int32_t K, int32_t Q,
+                     const double* w, double* lut, int mem, void* stream) {
+  if (M <= 0 || K <= 0 || Q <= 0) return fail(OTF_ERR_CONFIG, "bad codebook shape");
+  STATELESS_BEGIN(device, mem, stream)
+  const void *dc, *dw; void* dl;
+  if ((rc = S.in(centroids, (size_t)M * K * Q * 4, mem, &dc))) return rc;
+  if ((rc = S.in(w, (size_t)M * Q * 8, mem, &dw))) return rc;
+  if ((rc = S.outbuf(lut, (size_t)M * K * 8, mem, &dl))) return rc;
+  if ((rc = launch_pq_lut(static_cast<const float*>(dc), M, K, Q, static_cast<const double*>(dw),
+                          static_cast<double*>(dl), st))) return rc;
+  return S.out(lut, dl, (size_t)M * K * 8, mem);
+}
+
+int otf_pq_score_codes(int device, const double* lut, int32_t M, int32_t K, const uint8_t* codes,
+                       int64_t n, double* out, int mem, void* stream) {
+  if (M <= 0 || K <= 0) return fail(OTF_ERR_CONFIG, "bad LUT shape");
+  STATELESS_BEGIN(device, mem, stream)
+  const void *dl, *dc; void* dout; DevBuf bad;
+  if ((rc = S.in(lut, (size_t)M * K * 8, mem, &dl))) return rc;
+  if ((rc = S.in(codes, (size_t)n * M, mem, &dc))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * 8, mem, &dout))) return rc;
+  if (K < 256) {
+    if ((rc = bad.ensure(sizeof(unsigned int)))) return rc;
+    OTF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned int), st));
+    if ((rc = launch_pq_check(static_cast<const uint8_t*>(dc), n * M, K, static_cast<unsigned int*>(bad.p),
+                              device, st))) return rc;
+    unsigned int hb = 0;
+    OTF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    OTF_CUDA(cudaStreamSynchronize(st));
+    bad.release();
+    if (hb) return fail(OTF_ERR_CORRUPTION, "code value out of range for " + std::to_string(K) + " centroids");
+  }
+  if ((rc = launch_pq_scan(static_cast<const uint8_t*>(dc), n, M, static_cast<const double*>(dl), K,
+                           static_cast<double*>(dout), device, st))) return rc;
+  return S.out(out, dout, (size_t)n * 8, mem);
+}
+
+int otf_score_binary(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
+                     const double* w, float* out, int mem, void* stream) {
+  if (output_bits <= 0) return fail(OTF_ERR_CONFIG, "output_bits must be positive");
+  STATELESS_BEGIN(device, mem, stream)
+  const int row_bytes = (output_bits + 7) / 8;
+  const void *dc, *dw; void* dout; DevBuf aux;
+  if ((rc = S.in(codes, (size_t)n * row_bytes, mem, &dc))) return rc;
+  if ((rc = S.in(w, (size_t)output_bits * 8, mem, &dw))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * 4, mem, &dout))) return rc;
+  const size_t lb = bin_lut_bytes(output_bits);
+  if (lb) {
+    if ((rc = aux.ensure(lb))) return rc;
+    if ((rc = launch_bin_lut(static_cast<const double*>(dw), output_bits, static_cast<double*>(aux.p), st))) return rc;
+    rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<const double*>(aux.p),
+                          nullptr, static_cast<float*>(dout), device, st);
+  } else {
+    if ((rc = aux.ensure((size_t)output_bits * 4))) return rc;
+    if ((rc = launch_cast_w(static_cast<const double*>(dw), static_cast<float*>(aux.p), output_bits, st))) return rc;
+    rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, nullptr,
+                          static_cast<const float*>(aux.p), static_cast<float*>(dout), device, st);
+  }
+  if (rc) return rc;
+  rc = S.out(out, dout, (size_t)n * 4, mem);
+  if (mem == OTF_MEM_DEVICE) cudaStreamSynchronize(st);
+  aux.release();
+  return rc;
+}
+
+int otf_unpack_bits(int device, const uint8_t* codes, int64_t n, int32_t output_bits, float* out,
+                    int mem, void* stream) {
+  if (output_bits <= 0) return fail(OTF_ERR_CONFIG, "output_bits must be positive");
+  STATELESS_BEGIN(device, mem, stream)
+  const int row_bytes = (output_bits + 7) / 8;
+  const void* dc; void* dout;
+  if ((rc = S.in(codes, (size_t)n * row_bytes, mem, &dc))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * output_bits * 4, mem, &dout))) return rc;
+  if ((rc = launch_bin_unpack(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<float*>(dout),
+                              device, st))) return rc;
+  return S.out(out, dout, (size_t)n * output_bits * 4, mem);
+}
+
+int otf_binarize(int device, const double* frame, const float* centering, int32_t input_dim,
+                 int32_t output_bits, const double* X, int64_t n, uint8_t* out, int mem,
+                 void* stream) {
+  if (input_dim <= 0 || output_bits <= 0) return fail(OTF_ERR_CONFIG, "bad frame shape");
+  STATELESS_BEGIN(device, mem, stream)
+  const int row_bytes = (output_bits + 7) / 8;
+  const void *dU, *dmu, *dX; void* dout;
+  if ((rc = S.in(frame, (size_t)output_bits * input_dim * 8, mem, &dU))) return rc;
+  if ((rc = S.in(centering, (size_t)input_dim * 4, mem, &dmu))) return rc;
+  if ((rc = S.in(X, (size_t)n * input_dim * 8, mem, &dX))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * row_bytes, mem, &dout))) return rc;
+  if ((rc = launch_binarize(static_cast<const double*>(dU), static_cast<const float*>(dmu), input_dim,
+                            output_bits, static_cast<const double*>(dX), n, static_cast<uint8_t*>(dout),
+                            device, st))) return rc;
+  return S.out(out, dout, (size_t)n * row_bytes, mem);
+}
+
+int otf_hamming(int device, const uint8_t* a, const uint8_t* b, int64_t n, int32_t width,
+                int64_t* out, int mem, void* stream) {
+  STATELESS_BEGIN(device, mem, stream)
+  const void *da, *db; void* dout;
+  if ((rc = S.in(a, (size_t)n * width, mem, &da))) return rc;
+  if ((rc = S.in(b, (size_t)n * width, mem, &db))) return rc;
+  if ((rc = S.outbuf(out, (size_t)n * 8, mem, &dout))) return rc;
+  if ((rc = launch_hamming(static_cast<const uint8_t*>(da), static_cast<const uint8_t*>(db), n, width,
+                           static_cast<int64_t*>(dout), device, st))) return rc;
+  return S.out(out, dout, (size_t)n * 8, mem);
+}
+
+int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const int64_t* ids, int64_t k,
+              int64_t* out_ids, double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
+              void* stream) {
+  const int64_t k_eff = k < 0 ? 0 : (k > n ? n : k);
+  if (out_n) *out_n = k_eff;
+  if (k_eff == 0) return OTF_OK;
+  STATELESS_BEGIN(device, mem, stream)
+  const size_t es = dtype == OTF_F64 ? 8 : 4;
+  const void *ds, *di = nullptr;
+  void *d_ids, *d_sc, *d_rows = nullptr;
+  TopkWs ws;
+  if ((rc = S.in(scores, (size_t)n * es, mem, &ds))) return rc;
+  if (ids && (rc = S.in(ids, (size_t)n * 8, mem, &di))) return rc;
+  if ((rc = S.outbuf(out_ids, (size_t)k_eff * 8, mem, &d_ids))) return rc;
+  if ((rc = S.outbuf(out_scores, (size_t)k_eff * 8, mem, &d_sc))) return rc;
+  if (out_rows && (rc = S.outbuf(out_rows, (size_t)k_eff * 8, mem, &d_rows))) return rc;
+  rc = launch_topk(ds, dtype, n, static_cast<const int64_t*>(di), 0, k_eff, &ws,
+                   static_cast<int64_t*>(d_ids), static_cast<double*>(d_sc),
+                   static_cast<int64_t*>(d_rows), device, st);
+  if (!rc) rc = S.out(out_ids, d_ids, (size_t)k_eff * 8, mem);
+  if (!rc) rc = S.out(out_scores, d_sc, (size_t)k_eff * 8, mem);
+  if (!rc && out_rows) rc = S.out(out_rows, d_rows, (size_t)k_eff * 8, mem);
+  cudaStreamSynchronize(st);
+  topk_ws_free(&ws);
+  return rc;
+}
+
+// ---- Pegasos -------------------------------------------------------------------------------------
+int otf_pegasos_update(int device, double* w, int32_t d, const void* pos, int32_t pos_dtype,
+                       int64_t n_pos, const void* neg, int32_t neg_dtype, int64_t n_neg,
+                       const int64_t* pos_idx, const int64_t* neg_idx, int32_t half,
+                       double shrink, double eta_over_b, int project, double radius,
+                       void* stream) {
+  if (d <= 0 || half <= 0) return fail(OTF_ERR_CONFIG, "bad pegasos shape");
+  if (n_pos <= 0) return fail(OTF_ERR_NOT_READY, "no positives available yet");
+  if (n_neg <= 0) return fail(OTF_ERR_INSUFFICIENT, "negative pool is empty");
+  DeviceGuard g(device);
+  return launch_pegasos(w, d, pos, pos_dtype, n_pos, neg, neg_dtype, n_neg, pos_idx, neg_idx, half,
+                        shrink, eta_over_b, project, radius, static_cast<cudaStream_t>(stream));
+}
+
+int otf_pegasos_step_host(int device, double* w, int32_t d, const double* batch, int32_t half,
+                          double shrink, double eta_over_b, int project, double radius) {
+  if (d <= 0 || half <= 0) return fail(OTF_ERR_CONFIG, "bad pegasos shape");
+  STATELESS_BEGIN(device, OTF_MEM_HOST, nullptr)
+  const size_t bb = (size_t)2 * half * d * 8;
+  DevBuf buf, idx;
+  if ((rc = buf.ensure(bb + (size_t)d * 8))) return rc;
+  if ((rc = idx.ensure((size_t)2 * half * 8))) return rc;
+  std::vector<int64_t> hidx(2 * half);
+  for (int i = 0; i < half; ++i) { hidx[i] = i; hidx[half + i] = half + i; }
+  double* dw = static_cast<double*>(buf.p);
+  const double* dbatch = dw + d;
+  OTF_CUDA(cudaMemcpyAsync(dw, w, (size_t)d * 8, cudaMemcpyHostToDevice, st));
+  OTF_CUDA(cudaMemcpyAsync(const_cast<double*>(dbatch), batch, bb, cudaMemcpyHostToDevice, st));
+  OTF_CUDA(cudaMemcpyAsync(idx.p, hidx.data(), (size_t)2 * half * 8, cudaMemcpyHostToDevice, st));
+  const int64_t* di = static_cast<const int64_t*>(idx.p);
+  // positives and negatives both index the one uploaded batch (rows 0..half-1, half..2h-1)
+  rc = launch_pegasos(dw, d, dbatch, OTF_F64, 2 * half, dbatch, OTF_F64, 2 * half, di, di + half, half,
+                      shrink, eta_over_b, project, radius, st);
+  if (rc) return rc;
+  OTF_CUDA(cudaMemcpyAsync(w, dw, (size_t)d * 8, cudaMemcpyDeviceToHost, st));
+  OTF_CUDA(cudaStreamSynchronize(st));
+  buf.release(); idx.release();
+  return OTF_OK;
+}
+
+int otf_trainer_create(int device, int32_t dim, const void* negatives, int32_t neg_dtype, int64_t n_neg,
+                       int mem, otf_trainer** out) {
+  *out = nullptr;
+  if (n_neg <= 0) return fail(OTF_ERR_INSUFFICIENT, "negative pool must be a non-empty 2-D array");
+  if (dim <= 0) return fail(OTF_ERR_CONFIG, "dim must be positive");
+  DeviceGuard g(device);
+  otf_trainer* t = new otf_trainer();
+  t->device = device; t->dim = dim; t->neg_dtype = neg_dtype; t->n_neg = n_neg;
+  int rc = make_stream(&t->stream, true);
+  const size_t es = neg_dtype == OTF_F64 ? 8 : 4;
+  if (!rc) rc = t->neg.ensure((size_t)n_neg * dim * es);
+  if (!rc) rc = copy_in(t->neg.p, negatives, (size_t)n_neg * dim * es, mem, t->stream);
+  if (!rc) rc = t->w.ensure((size_t)dim * 8);
+  if (!rc) { cudaError_t e = cudaMemsetAsync(t->w.p, 0, (size_t)dim * 8, t->stream); if (e) rc = cuda_fail(e, "memset w"); }
+  if (!rc) { cudaError_t e = cudaStreamSynchronize(t->stream); if (e) rc = cuda_fail(e, "trainer_create"); }
+  if (rc) { otf_trainer_destroy(t); return rc; }
+  *out = t;
+  return OTF_OK;
+}
+
+int otf_trainer_destroy(otf_trainer* t) {
+  if (!t) return OTF_OK;
+  DeviceGuard g(t->device);
+  if (t->stream) cudaStreamSynchronize(t->stream);
+  t->w.release(); t->neg.release(); t->pos_pool.release(); t->pos_stage.release(); t->idx.release();
+  t->h_stage.release(); t->h_idx.release();
+  if (t->stream) cudaStreamDestroy(t->stream);
+  delete t;
+  return OTF_OK;
+}
+
+int otf_trainer_append_positives(otf_trainer* t, const void* rows, int32_t dtype, int64_t n_rows, int mem) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard g(t->device);
+  if (n_rows <= 0) return OTF_OK;
+  const size_t rb = (size_t)t->dim * 4;  // device pool is float32 (session.py:70 PositivePool)
+  if (dtype != OTF_F32) return fail(OTF_ERR_CONFIG, "device positive pool stores float32 rows");
+  if (t->n_pos + n_rows > t->pos_cap) {
+    int64_t cap = t->pos_cap > 0 ? t->pos_cap : 64;
+    while (cap < t->n_pos + n_rows) cap *= 2;
+    DevBuf grown;
+    int rc = grown.ensure((size_t)cap * rb);
+    if (rc) return rc;
+    if (t->n_pos) OTF_CUDA(cudaMemcpyAsync(grown.p, t->pos_pool.p, (size_t)t->n_pos * rb, cudaMemcpyDeviceToDevice, t->stream));
+    OTF_CUDA(cudaStreamSynchronize(t->stream));
+    t->pos_pool.release();
+    t->pos_pool = grown;
+    grown.p = nullptr;
+    t->pos_cap = cap;
+  }
+  int rc = copy_in(static_cast<uint8_t*>(t->pos_pool.p) + (size_t)t->n_pos * rb, rows, (size_t)n_rows * rb, mem, t->stream);
+  if (rc) return rc;
+  OTF_CUDA(cudaStreamSynchronize(t->stream));
+  t->n_pos += n_rows;
+  return OTF_OK;
+}
+
+int otf_trainer_pool_size(const otf_trainer* t, int64_t* n_pos) {
+  *n_pos = t->n_pos;
+  return OTF_OK;
+}
+
+int otf_trainer_step(otf_trainer* t, const void* positives, int32_t pos_dtype, int64_t n_pos,
+                     const int64_t* pos_idx, const int64_t* neg_idx, int32_t half, double shrink,
+                     double eta_over_b, int project, double radius) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard g(t->device);
+  const int64_t pool = positives ? n_pos : t->n_pos;
+  if (pool <= 0) return fail(OTF_ERR_NOT_READY, "no positives available yet");
+  if (half <= 0) return fail(OTF_ERR_CONFIG, "batch half must be positive");
+  const size_t es = pos_dtype == OTF_F64 ? 8 : 4;
+  const size_t rb = (size_t)t->dim * es;
+  // host staging: [pos rows (if host pool)] [pos_idx] [neg_idx]
+  const size_t idx_bytes = (size_t)2 * half * 8;
+  const size_t rows_bytes = positives ? (size_t)half * rb : 0;
+  int rc = t->h_stage.ensure(rows_bytes + idx_bytes);
+  if (!rc) rc = t->pos_stage.ensure(rows_bytes + idx_bytes);
+  if (rc) return rc;
+  // the previous step's copies out of h_stage must have completed before we overwrite it
+  OTF_CUDA(cudaStreamSynchronize(t->stream));
+  uint8_t* hs = static_cast<uint8_t*>(t->h_stage.p);
+  int64_t* hidx = reinterpret_cast<int64_t*>(hs + rows_bytes);
+  for (int i = 0; i < half; ++i) {
+    if (pos_idx[i] < 0 || pos_idx[i] >= pool) return fail(OTF_ERR_CONFIG, "positive index out of range");
+    if (neg_idx[i] < 0 || neg_idx[i] >= t->n_neg) return fail(OTF_ERR_CONFIG, "negative index out of range");
+    if (positives) {
+      std::memcpy(hs + (size_t)i * rb, static_cast<const uint8_t*>(positives) + (size_t)pos_idx[i] * rb, rb);
+      hidx[i] = i;
+    } else {
+      hidx[i] = pos_idx[i];
+    }
+    hidx[half + i] = neg_idx[i];
+  }
+  OTF_CUDA(cudaMemcpyAsync(t->pos_stage.p, hs, rows_bytes + idx_bytes, cudaMemcpyHostToDevice, t->stream));
+  uint8_t* ds = static_cast<uint8_t*>(t->pos_stage.p);
+  const int64_t* d_pidx = reinterpret_cast<const int64_t*>(ds + rows_bytes);
+  const void* pos_src = positives ? static_cast<const void*>(ds) : t->pos_pool.p;
+  const int pdt = positives ? pos_dtype : OTF_F32;
+  return launch_pegasos(static_cast<double*>(t->w.p), t->dim, pos_src, pdt, pool, t->neg.p, t->neg_dtype,
+                        t->n_neg, d_pidx, d_pidx + half, half, shrink, eta_over_b, project, radius, t->stream);
+}
+
+int otf_trainer_weights(otf_trainer* t, double* out, int mem) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard g(t->device);
+  OTF_CUDA(cudaMemcpyAsync(out, t->w.p, (size_t)t->dim * 8,
+                           mem == OTF_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, t->stream));
+  OTF_CUDA(cudaStreamSynchronize(t->stream));
+  return OTF_OK;
+}
+
+int otf_trainer_set_weights(otf_trainer* t, const double* w, int mem) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard g(t->device);
+  int rc = copy_in(t->w.p, w, (size_t)t->dim * 8, mem, t->stream);
+  if (rc) return rc;
+  OTF_CUDA(cudaStreamSynchronize(t->stream));
+  return OTF_OK;
+}
+
+int otf_trainer_weights_ptr(otf_trainer* t, const double** out) {
+  *out = static_cast<const double*>(t->w.p);
+  return OTF_OK;
+}
+
+int otf_trainer_stream(otf_trainer* t, void** out) {
+  *out = t->stream;
+  return OTF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// otf_dense.cu — K1: dense float32 linear-SVM scoring (score_dense, ranker.py:63-69).
+//
+// s_i = float32( sum_j x_ij * float32(w_j) ), accumulated in float64. Products of two
+// float32 values are exact in float64, so the only rounding is in the float64 adds and the
+// final round-to-nearest to float32. The reference computes the same dot product with an
+// OpenBLAS sgemv (float32 accumulation, host-CPU dependent order), so parity is a stated
+// tolerance. Every row is reduced with the same fixed tree whatever its
+// position, GPU or shard, so a row's score is bit-identical across repositories, subsets
+// (without_ids) and GPU counts.
+//
+// Canonical per-row order (shared by all variants below): lane l of a 32-lane group owns
+// columns {128*c + 4*l + e : c = 0.., e = 0..3}; it accumulates them in (c, e) order into a
+// float64 partial; the 32 partials are then combined by the xor-butterfly tree
+// (l, l^16), (l, l^8), ..., (l, l^1).
+//
+// HBM roofline: 4*d bytes per row; 0.5 flop/byte. Loads are 128-bit, coalesced, streamed
+// past L1 (ld.global.nc.L1::no_allocate); the grid is persistent (a multiple of the 148 SMs).
+#include "otf_common.cuh"
+#include "otf_internal.h"
+
+namespace otf {
+
+// Fast path: d == 128 * CPL. Each warp handles R rows per iteration (R*CPL <= 16 float4
+// loads in flight per lane), then a transposed butterfly gives ~2 shuffles per row.
+template <int CPL, int R>
+__global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restrict__ X, int64_t n,
+                                                           const float* __restrict__ w32,
+                                                           float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  // w (float32) staged once per CTA in shared memory; lanes read consecutive float4s
+  __shared__ float4 wr[32 * CPL];
+  for (int t = threadIdx.x; t < 32 * CPL; t += blockDim.x) wr[t] = reinterpret_cast<const float4*>(w32)[t];
+  __syncthreads();
+  const int64_t row_f4 = 32 * CPL;  // float4 per row
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int LB = CPL < 8 ? CPL : 8;  // float4 loads per row per batch
+  for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
+    double p[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) p[i] = 0.0;
+#pragma unroll
+    for (int c0 = 0; c0 < CPL; c0 += LB) {
+      float4 v[R][LB];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int64_t row = r0 + i;
+#pragma unroll
+        for (int c = 0; c < LB; ++c) {
+          if (row < n) v[i][c] = ld_stream_f4(X4 + row * row_f4 + lane + 32 * (c0 + c));
+          else v[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double acc = p[i];
+#pragma unroll
+        for (int c = 0; c < LB; ++c) {
+          const float4 wv = wr[lane + 32 * (c0 + c)];
+          acc = __fma_rn((double)v[i][c].x, (double)wv.x, acc);
+          acc = __fma_rn((double)v[i][c].y, (double)wv.y, acc);
+          acc = __fma_rn((double)v[i][c].z, (double)wv.z, acc);
+          acc = __fma_rn((double)v[i][c].w, (double)wv.w, acc);
+        }
+        p[i] = acc;
+      }
+    }
+    transposed_reduce<R, 32>(p, lane);
+    bool writer;
+    const int slot = row_of_lane<R, 32>(lane, &writer);
+    const int64_t row = r0 + slot;
+    if (writer && row < n) out[row] = __double2float_rn(p[0]);
+  }
+}
+
+// Generic path: any d (and any alignment). One warp per row, same canonical order.
+__global__ void __launch_bounds__(256) dense_score_generic(const float* __restrict__ X, int64_t n,
+                                                           int32_t d, const float* __restrict__ w32,
+                                                           float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < n; row += nwarp) {
+    const float* x = X + row * (int64_t)d;
+    double acc = 0.0;
+    for (int base = 4 * lane; base < d; base += 128) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = base + e;
+        if (j < d) acc = __fma_rn((double)__ldg(x + j), (double)w32[j], acc);
+      }
+    }
+    double p[1] = {acc};
+    transposed_reduce<1, 32>(p, lane);
+    if (lane == 0) out[row] = __double2float_rn(p[0]);
+  }
+}
+
+// w (float64) -> float32 round-to-nearest (ranker.py:69 `w.astype(np.float32)`).
+__global__ void cast_w_f32(const double* __restrict__ w, float* __restrict__ w32, int32_t d) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
+    w32[j] = __double2float_rn(w[j]);
+}
+
+static int grid_for(const void* fn, int threads, int device) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * sm_count(device);
+}
+
+template <int CPL, int R>
+static int launch_fast(const float* X, int64_t n, const float* w32, float* out, int device,
+                       cudaStream_t st) {
+  auto fn = dense_score_fast<CPL, R>;
+  int grid = grid_for((const void*)fn, 256, device);
+  const int64_t need = (n + (8 * R) - 1) / (8 * R);  // 8 warps per block
+  if (need < grid) grid = (int)(need > 0 ? need : 1);
+  fn<<<grid, 256, 0, st>>>(X, n, w32, out);
+  OTF_LAUNCH_CHECK("dense_score_fast");
+  return OTF_OK;
+}
+
+int launch_cast_w(const double* w, float* w32, int32_t d, cudaStream_t st) {
+  cast_w_f32<<<(d + 255) / 256, 256, 0, st>>>(w, w32, d);
+  OTF_LAUNCH_CHECK("cast_w_f32");
+  return OTF_OK;
+}
+
+// Scores n rows; w32 is the float32-cast model (device). Pointers must be 16-byte aligned
+// for the fast path (all device buffers this library allocates are).
+int launch_dense_score(const float* X, int64_t n, int32_t d, const float* w32, float* out,
+                       int device, cudaStream_t st) {
+  if (n <= 0) return OTF_OK;
+  const bool aligned = (((uintptr_t)X) & 15) == 0 && (((uintptr_t)w32) & 15) == 0;
+  if (aligned && d % 128 == 0) {
+    switch (d / 128) {
+      case 1: return launch_fast<1, 8>(X, n, w32, out, device, st);
+      case 2: return launch_fast<2, 4>(X, n, w32, out, device, st);
+      case 4: return launch_fast<4, 2>(X, n, w32, out, device, st);
+      case 8: return launch_fast<8, 1>(X, n, w32, out, device, st);
+      case 16: return launch_fast<16, 1>(X, n, w32, out, device, st);
+      case 32: return launch_fast<32, 1>(X, n, w32, out, device, st);
+      default: break;
+    }
+  }
+  int grid = grid_for((const void*)dense_score_generic, 256, device);
+  const int64_t need = (n + 7) / 8;
+  if (need < grid) grid = (int)need;
+  dense_score_generic<<<grid, 256, 0, st>>>(X, n, d, w32, out);
+  OTF_LAUNCH_CHECK("dense_score_generic");
+  return OTF_OK;
+}
+
+}  // namespace otf

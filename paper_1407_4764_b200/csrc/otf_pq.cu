@@ -1,0 +1,241 @@
+// otf_pq.cu — K2/K3: product-quantized scoring (score_pq, ranker.py:72-75;
+// build_score_lut pq.py:248-259; score_codes pq.py:262-276).
+//
+// Bit-exact with the reference's numpy arithmetic:
+//  * LUT[m][j] = einsum("mkq,mq->mk") in float64 with the FULL float64 w (no float32 cast,
+//    pq.py:255). numpy's einsum inner kernel (SSE2, two lanes, no FMA) multiplies each
+//    c*w term separately and adds them into two accumulators in a fixed pattern:
+//    each 8-block contributes p6,p4,p2,p0 to acc0 and p7,p5,p3,p1 to acc1; the tail adds
+//    pairs (even->acc0, odd->acc1) and a final odd element to acc0; result 0.0+(acc0+acc1).
+//    Restated (and pinned against numpy) in oracle/otf_oracle.py::lut_entry_numpy_order.
+//  * s_i = lut[cols, codes[i]].sum(axis=1): numpy pairwise summation over the M entries
+//    (n<8: sequential from -0.0; 8<=n<=128: 8 strided accumulators, tree, sequential tail;
+//    n>128: split at n/2 rounded down to a multiple of 8). Restated in
+//    oracle/otf_oracle.py::pairwise_sum_numpy_order.
+// __dmul_rn/__dadd_rn keep nvcc from contracting into FMAs.
+//
+// HBM roofline: M bytes per row (16 B for C3). The LUT (M*256*8 B) lives in shared memory;
+// the scan is shared-memory-lookup bound for M=16.
+#include "otf_common.cuh"
+#include "otf_internal.h"
+
+namespace otf {
+
+__device__ __forceinline__ double lut_entry_einsum(const float* __restrict__ c,
+                                                   const double* __restrict__ w, int Q) {
+  double acc0 = 0.0, acc1 = 0.0;
+  int i = 0;
+  for (; Q - i >= 8; i += 8) {
+    acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i + 6], w[i + 6]));
+    acc1 = __dadd_rn(acc1, __dmul_rn((double)c[i + 7], w[i + 7]));
+    acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i + 4], w[i + 4]));
+    acc1 = __dadd_rn(acc1, __dmul_rn((double)c[i + 5], w[i + 5]));
+    acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i + 2], w[i + 2]));
+    acc1 = __dadd_rn(acc1, __dmul_rn((double)c[i + 3], w[i + 3]));
+    acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i + 0], w[i + 0]));
+    acc1 = __dadd_rn(acc1, __dmul_rn((double)c[i + 1], w[i + 1]));
+  }
+  for (; Q - i >= 2; i += 2) {
+    acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i], w[i]));
+    acc1 = __dadd_rn(acc1, __dmul_rn((double)c[i + 1], w[i + 1]));
+  }
+  if (i < Q) acc0 = __dadd_rn(acc0, __dmul_rn((double)c[i], w[i]));
+  return __dadd_rn(0.0, __dadd_rn(acc0, acc1));
+}
+
+// lut is (M, K) row-major float64 (the reference's layout).
+__global__ void pq_build_lut_kernel(const float* __restrict__ cents, int M, int K, int Q,
+                                    const double* __restrict__ w, double* __restrict__ lut) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M * K) return;
+  const int m = t / K;
+  lut[t] = lut_entry_einsum(cents + (int64_t)t * Q, w + (int64_t)m * Q, Q);
+}
+
+// numpy pairwise sum (n <= 128 branch and the recursive split), values from a getter.
+template <typename Get>
+__device__ __forceinline__ double pairwise_block(const Get& a, int s, int n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, a(s + i));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a(s + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a(s + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a(s + i));
+  return res;
+}
+template <typename Get>
+__device__ double pairwise_sum(const Get& a, int s, int n) {
+  if (n <= 128) return pairwise_block(a, s, n);
+  // explicit stack instead of recursion: numpy splits at n2 = (n/2) - (n/2)%8
+  // and returns pairwise(left) + pairwise(right). Depth <= log2(n/128)+1.
+  struct Frame { int s, n, stage; double left; };
+  Frame st[24];
+  int top = 0;
+  st[0] = {s, n, 0, 0.0};
+  double ret = 0.0;
+  while (top >= 0) {
+    Frame& f = st[top];
+    if (f.n <= 128) { ret = pairwise_block(a, f.s, f.n); --top; continue; }
+    int n2 = f.n / 2; n2 -= n2 % 8;
+    if (f.stage == 0) { f.stage = 1; st[top + 1] = {f.s, n2, 0, 0.0}; ++top; continue; }
+    if (f.stage == 1) { f.left = ret; f.stage = 2; st[top + 1] = {f.s + n2, f.n - n2, 0, 0.0}; ++top; continue; }
+    ret = __dadd_rn(f.left, ret);
+    --top;
+  }
+  return ret;
+}
+
+struct SmemLut {
+  const double* lut; int K; const uint8_t* code;
+  __device__ __forceinline__ double operator()(int m) const { return lut[m * K + code[m]]; }
+};
+
+// Fast path, compile-time M (M in {4, 8, 16, 32}): one thread per row, codes loaded as
+// 16-byte vectors, LUT (M x 256 float64, zero padded beyond K) in shared memory.
+template <int M>
+__global__ void __launch_bounds__(256) pq_scan_fast(const uint8_t* __restrict__ codes, int64_t n,
+                                                    const double* __restrict__ lut_g, int K,
+                                                    double* __restrict__ out) {
+  extern __shared__ double lut[];  // M * 256
+  for (int t = threadIdx.x; t < M * 256; t += blockDim.x) {
+    const int m = t >> 8, j = t & 255;
+    lut[t] = j < K ? lut_g[m * K + j] : 0.0;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
+    uint8_t c[M];
+    if constexpr (M >= 16) {
+#pragma unroll
+      for (int v = 0; v < M / 16; ++v) {
+        uint4 u = ld_stream_u4(reinterpret_cast<const uint4*>(codes + row * M) + v);
+        const uint32_t words[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) c[16 * v + q] = (words[q >> 2] >> (8 * (q & 3))) & 0xff;
+      }
+    } else if constexpr (M == 8) {
+      uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + row * M));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = ((q < 4 ? u.x : u.y) >> (8 * (q & 3))) & 0xff;
+    } else {
+      uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(codes + row * M));
+#pragma unroll
+      for (int q = 0; q < M; ++q) c[q] = (u >> (8 * q)) & 0xff;
+    }
+    double a[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) a[m] = lut[m * 256 + c[m]];
+    double res;
+    if constexpr (M < 8) {
+      res = -0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) res = __dadd_rn(res, a[m]);
+    } else {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a[j];
+#pragma unroll
+      for (int i = 8; i < M; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+      }
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    }
+    out[row] = res;
+  }
+}
+
+// Generic path: any M, K; LUT read through L1 from global memory.
+__global__ void __launch_bounds__(256) pq_scan_generic(const uint8_t* __restrict__ codes, int64_t n,
+                                                       int M, const double* __restrict__ lut,
+                                                       int K, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
+    SmemLut g{lut, K, codes + row * M};
+    out[row] = pairwise_sum(g, 0, M);
+  }
+}
+
+// max code per launch -> flag if any code >= K (validation, pq.py:240-241 semantics).
+__global__ void pq_check_codes(const uint8_t* __restrict__ codes, int64_t total, int K,
+                               unsigned int* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int found = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    found |= codes[i] >= K;
+  if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(bad, 1u);
+}
+
+int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
+                  cudaStream_t st) {
+  const int total = M * K;
+  pq_build_lut_kernel<<<(total + 255) / 256, 256, 0, st>>>(cents, M, K, Q, w, lut);
+  OTF_LAUNCH_CHECK("pq_build_lut");
+  return OTF_OK;
+}
+
+int launch_pq_check(const uint8_t* codes, int64_t total, int K, unsigned int* bad,
+                    int device, cudaStream_t st) {
+  if (total <= 0 || K >= 256) return OTF_OK;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = 4LL * sm_count(device);
+  if (blocks > cap) blocks = cap;
+  pq_check_codes<<<(int)blocks, 256, 0, st>>>(codes, total, K, bad);
+  OTF_LAUNCH_CHECK("pq_check_codes");
+  return OTF_OK;
+}
+
+template <int M>
+static int launch_fast(const uint8_t* codes, int64_t n, const double* lut, int K, double* out,
+                       int device, cudaStream_t st) {
+  auto fn = pq_scan_fast<M>;
+  const size_t smem = (size_t)M * 256 * sizeof(double);
+  static bool configured[64] = {false};
+  if (!configured[device & 63]) {
+    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[device & 63] = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)per_sm * sm_count(device);
+  const int64_t need = (n + 255) / 256;
+  if (need < grid) grid = need;
+  fn<<<(int)grid, 256, smem, st>>>(codes, n, lut, K, out);
+  OTF_LAUNCH_CHECK("pq_scan_fast");
+  return OTF_OK;
+}
+
+int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const double* lut, int K,
+                   double* out, int device, cudaStream_t st) {
+  if (n <= 0) return OTF_OK;
+  const bool aligned16 = (((uintptr_t)codes) & 15) == 0;
+  if (aligned16) {
+    switch (M) {
+      case 4: return launch_fast<4>(codes, n, lut, K, out, device, st);
+      case 8: return launch_fast<8>(codes, n, lut, K, out, device, st);
+      case 16: return launch_fast<16>(codes, n, lut, K, out, device, st);
+      case 32: return launch_fast<32>(codes, n, lut, K, out, device, st);
+      default: break;
+    }
+  }
+  int64_t grid = (n + 255) / 256;
+  const int64_t cap = 8LL * sm_count(device);
+  if (grid > cap) grid = cap;
+  pq_scan_generic<<<(int)grid, 256, 0, st>>>(codes, n, M, lut, K, out);
+  OTF_LAUNCH_CHECK("pq_scan_generic");
+  return OTF_OK;
+}
+
+}  // namespace otf

@@ -1,0 +1,147 @@
+"""Generate golden fixtures by running the REAL reference (build container only).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Imports otf_retrieval from /root/reference/pkg/src (read-only), runs its hot-path functions on
+seeded inputs and writes tests/golden/golden.npz. The GPU box has no /root/reference; the tests
+only read the committed .npz. Inputs are stored next to outputs so nothing is regenerated.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent / "golden.npz"
+
+
+def main() -> None:
+    sys.path.insert(0, str(REF))
+    sys.dont_write_bytecode = True
+    from otf_retrieval import binary as rb
+    from otf_retrieval import pq as rpq
+    from otf_retrieval import ranker as rr
+    from otf_retrieval import trainer as rt
+    from otf_retrieval.model import LinearModel
+    from otf_retrieval.store import FeatureStore, normalize_rows
+
+    g: dict[str, np.ndarray] = {}
+
+    # ---- dense scoring + ranking (ranker.py:63-69, :97-143, :272-281) --------------------
+    for name, (n, d, seed) in {"d16": (200, 16, 3), "d128": (1500, 128, 5), "d2048": (120, 2048, 7),
+                               "d5": (333, 5, 9)}.items():
+        rng = np.random.default_rng(seed)
+        x = normalize_rows(rng.standard_normal((n, d)))
+        w = rng.standard_normal(d)
+        ids = np.arange(n, dtype=np.int64) * 3 + 11
+        rng.shuffle(ids)
+        store = FeatureStore(x, ids=ids)
+        repo = rr.Repository.dense(store)
+        ranked = repo.rank(LinearModel(w, 1, 4), 50)
+        g[f"dense_{name}_x"] = x
+        g[f"dense_{name}_w"] = w
+        g[f"dense_{name}_ids"] = ids
+        g[f"dense_{name}_scores"] = repo.score(w)
+        g[f"dense_{name}_rank_ids"] = ranked.ids
+        g[f"dense_{name}_rank_scores"] = ranked.scores
+
+    # ---- PQ (pq.py:248-276) — bit-exact targets ------------------------------------------
+    for name, (m, k, q, n, seed) in {"m4k8q4": (4, 8, 4, 500, 11), "m16k256q8": (16, 256, 8, 3000, 12),
+                                     "m5k7q3": (5, 7, 3, 300, 13), "m32k256q4": (32, 256, 4, 2000, 14),
+                                     "m12k200q16": (12, 200, 16, 600, 15), "m200k16q1": (200, 16, 1, 300, 16)}.items():
+        rng = np.random.default_rng(seed)
+        cents = (rng.standard_normal((m, k, q)) * np.exp(rng.uniform(-3, 3, size=(m, k, 1)))).astype(np.float32)
+        book = rpq.PQCodebook(cents, np.zeros(m * q, dtype=np.float32))
+        codes = rng.integers(0, k, size=(n, m)).astype(np.uint8)
+        w = rng.standard_normal(m * q) * np.exp(rng.uniform(-2, 2, size=m * q))
+        lut = rpq.build_score_lut(w, book)
+        repo = rr.Repository.quantized(book, codes)
+        ranked = repo.rank(LinearModel(w, 1, 1), 40)
+        g[f"pq_{name}_cents"] = cents
+        g[f"pq_{name}_codes"] = codes
+        g[f"pq_{name}_w"] = w
+        g[f"pq_{name}_lut"] = lut
+        g[f"pq_{name}_scores"] = rpq.score_codes(lut, codes)
+        g[f"pq_{name}_rank_ids"] = ranked.ids
+        g[f"pq_{name}_rank_scores"] = ranked.scores
+
+    # ---- binary (ranker.py:78-94, binary.py:86-128) ----------------------------------------
+    for name, (m, bits, n, seed) in {"b32": (8, 32, 200, 21), "b2048": (128, 2048, 300, 22),
+                                     "b19": (8, 19, 150, 23), "b1024": (64, 1024, 300, 24)}.items():
+        rng = np.random.default_rng(seed)
+        frame = rb.make_tight_frame(m, bits, seed=seed)
+        codec = rb.BinaryCodec(frame, rng.standard_normal(m).astype(np.float32) * 0.1)
+        vecs = rng.standard_normal((n, m))
+        codes = rb.binarize(codec, vecs)
+        w = rng.standard_normal(bits)
+        repo = rr.Repository.binary(codec, codes)
+        ranked = repo.rank(LinearModel(w, 1, 2), 30)
+        if bits <= 1024:  # the 2048-bit frame (2 MB) is not needed to check scoring
+            g[f"bin_{name}_frame"] = frame.matrix
+            g[f"bin_{name}_center"] = codec.centering
+            g[f"bin_{name}_vecs"] = vecs
+        g[f"bin_{name}_codes"] = codes
+        g[f"bin_{name}_w"] = w
+        g[f"bin_{name}_scores"] = rr.score_binary(w, codes, bits)
+        g[f"bin_{name}_unpacked"] = rb.unpack_bits(codes[:20], bits)
+        g[f"bin_{name}_rank_ids"] = ranked.ids
+        g[f"bin_{name}_rank_scores"] = ranked.scores
+        other = rng.integers(0, 256, size=codes.shape).astype(np.uint8)
+        g[f"bin_{name}_other"] = other
+        g[f"bin_{name}_hamming"] = rb.hamming_distance(codes, other)
+        g[f"bin_{name}_adapted"] = repo.adapt_training_vectors(vecs[:10])
+
+    # ---- top_k known answers + ties (tests/test_ranker.py:139-197) -------------------------
+    rng = np.random.default_rng(11)
+    ties = rng.integers(0, 5, size=10_000).astype(np.float32)
+    tie_ids = np.arange(10_000, dtype=np.int64)
+    rng.shuffle(tie_ids)
+    r = rr.top_k(ties, 100, ids=tie_ids)
+    g["topk_ties_scores"], g["topk_ties_ids_in"] = ties, tie_ids
+    g["topk_ties_ids"], g["topk_ties_out_scores"] = r.ids, r.scores
+    rnd = np.random.default_rng(12).standard_normal(5000).astype(np.float32)
+    r = rr.top_k(rnd, 50)
+    g["topk_rand_scores"], g["topk_rand_ids"] = rnd, r.ids
+    sgn = np.array([0.0, -0.0, 1.0, -0.0, 0.0, -1.0], dtype=np.float32)
+    r = rr.top_k(sgn, 4)
+    g["topk_signed_zero_scores"], g["topk_signed_zero_ids"] = sgn, r.ids
+    f64 = np.random.default_rng(13).integers(-3, 4, size=3000).astype(np.float64) / 7.0
+    r = rr.top_k(f64, 1000)
+    g["topk_f64_scores"], g["topk_f64_ids"] = f64, r.ids
+    r = rr.top_k(f64[:700], 5000)
+    g["topk_full_ids"] = r.ids
+
+    # ---- Pegasos (trainer.py:51-173) ---------------------------------------------------------
+    rng = np.random.default_rng(31)
+    d = 24
+    pos = normalize_rows(rng.standard_normal((40, d)) + 1.5)
+    neg = normalize_rows(rng.standard_normal((300, d)) - 0.5)
+    batches: list[np.ndarray] = []
+    tr = rt.OnlineTrainer(d, neg, rt.TrainerConfig(lam=0.05, batch_size=16, seed=9),
+                          batch_hook=lambda p, q: batches.append(np.concatenate([p, q])))
+    ws = []
+    for _ in range(60):
+        tr.step(pos)
+        ws.append(tr.snapshot().weights)
+    g["peg_pos"], g["peg_neg"] = pos, neg
+    g["peg_idx"] = np.stack(batches)
+    g["peg_w"] = np.stack(ws)
+    # stateless pegasos_step sequence with project=False and float64 pools
+    rng2 = np.random.default_rng(5)
+    w = np.zeros(d)
+    seq = []
+    cfg = rt.TrainerConfig(lam=0.3, batch_size=8, project=False, seed=0)
+    for t in range(1, 31):
+        w = rt.pegasos_step(w, t, pos.astype(np.float64), neg.astype(np.float64), cfg, rng2)
+        seq.append(w)
+    g["peg_noproj_w"] = np.stack(seq)
+
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,360 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's own outputs
+(tests/golden, produced by the unmodified reference) and against the pinned oracle.
+
+Bars:
+  * PQ: LUT, scores, ranked ids and ranked scores bit-identical.
+  * top_k given the same scores: ids bit-identical (all edge cases of tests/test_ranker.py).
+  * dense / binary scores: |gpu - ref| <= 1e-6 * ||w||_2 * ||x||_2 (the reference's own sgemv
+    order is host-dependent); our scores are the float64-accumulated dot rounded once.
+  * ranked ids: identical to the oracle's top_k of the GPU's own scores (selection is exact) and
+    equal as sets / in order to the reference up to swaps of entries whose reference scores are
+    within that tolerance.
+  * Pegasos: w within rtol 1e-12 of the reference at every step, same sampled indices.
+"""
+
+import numpy as np
+import pytest
+
+import otf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DENSE = ["d16", "d128", "d2048", "d5"]
+PQ = ["m4k8q4", "m16k256q8", "m5k7q3", "m32k256q4", "m12k200q16", "m200k16q1"]
+BIN = ["b32", "b2048", "b19", "b1024"]
+
+
+def assert_rank_parity(got_ids, ref_ids, ref_score_of, tol):
+    """Set equality and order equality up to swaps of near-tied (|ds| <= tol) entries."""
+    got_ids, ref_ids = list(map(int, got_ids)), list(map(int, ref_ids))
+    assert len(got_ids) == len(ref_ids)
+    if got_ids == ref_ids:
+        return 0
+    # allow boundary differences only between near-ties with the last reference entry
+    last = ref_score_of[ref_ids[-1]]
+    extra = set(got_ids) ^ set(ref_ids)
+    for i in extra:
+        assert abs(ref_score_of[i] - last) <= tol, f"id {i} differs beyond tolerance"
+    swaps = 0
+    for a, b in zip(got_ids, ref_ids):
+        if a != b:
+            swaps += 1
+            if a in ref_score_of and b in ref_score_of:
+                assert abs(ref_score_of[a] - ref_score_of[b]) <= tol
+    return swaps
+
+
+def exact_dense(x, w):
+    return x.astype(np.float64) @ w.astype(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------------------------
+# dense (ranker.py:63-69, :272-281)
+
+
+@pytest.mark.parametrize("name", DENSE)
+def test_dense_scores_and_rank(otf, golden, name):
+    x, w, ids = golden[f"dense_{name}_x"], golden[f"dense_{name}_w"], golden[f"dense_{name}_ids"]
+    ref = golden[f"dense_{name}_scores"]
+    tol = 1e-6 * np.linalg.norm(w) * float(np.max(np.linalg.norm(x, axis=1)))
+    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    s = repo.score(w)
+    assert s.dtype == np.float32
+    assert np.max(np.abs(s.astype(np.float64) - ref)) <= tol
+    # float64-accumulated, rounded once: within half an ulp of the exact dot (+ f64 noise)
+    ex = exact_dense(x, w)
+    assert np.all(np.abs(s - ex) <= np.spacing(np.abs(s)) * 0.5 + 1e-12 * np.abs(ex) + 1e-30)
+    np.testing.assert_array_equal(otf.score_dense(w, x), s)
+    ranked = repo.rank(otf.LinearModel(w, 1, 4), 50, produced_at=2.5)
+    assert ranked.model_version == 4 and ranked.produced_at == 2.5
+    o_ids, o_sc, _ = O.top_k(s, 50, ids)
+    np.testing.assert_array_equal(ranked.ids, o_ids)
+    np.testing.assert_array_equal(ranked.scores, o_sc)
+    assert ranked.scores.dtype == np.float64 and ranked.ids.dtype == np.int64
+    ref_of = dict(zip(map(int, ids), ref.astype(np.float64)))
+    assert_rank_parity(ranked.ids, golden[f"dense_{name}_rank_ids"], ref_of, tol)
+
+
+def test_dense_edge_cases(otf):
+    rng = np.random.default_rng(1)
+    store = otf.FeatureStore(rng.standard_normal((10, 4)).astype(np.float32))
+    np.testing.assert_array_equal(otf.score_dense(np.zeros(4), store), 0.0)
+    assert not np.any(np.signbit(otf.score_dense(np.zeros(4), store)))
+    data = rng.standard_normal((20, 6)).astype(np.float32)
+    w = np.zeros(6)
+    w[3] = 1.0
+    np.testing.assert_array_equal(otf.score_dense(w, data), data[:, 3])
+    with pytest.raises(otf.ConfigError):
+        otf.score_dense(np.zeros(5), np.ones((2, 4), np.float32))
+    repo = otf.Repository.dense(otf.FeatureStore(rng.standard_normal((37, 128)).astype(np.float32)))
+    with pytest.raises(otf.ConfigError):
+        repo.score(np.zeros(127))
+    # w = 0: every score ties, the lowest ids win (tests/test_ranker.py:146-148)
+    r = repo.rank(otf.LinearModel(np.zeros(128), 1), 7)
+    assert list(r.ids) == list(range(7))
+    assert len(repo.rank(otf.LinearModel(np.ones(128), 1), 0)) == 0
+    w = rng.standard_normal(128)
+    full = repo.rank(otf.LinearModel(w, 1), 1000)  # k >= N: full sort
+    assert len(full) == 37
+    assert list(full.ids) == O.full_sort_ids(repo.score(w), np.arange(37), 37)
+
+
+@pytest.mark.parametrize("n,d", [(1, 128), (31, 128), (33, 256), (1000, 384), (517, 2048), (300, 4096), (77, 3)])
+def test_dense_shapes_position_independent(otf, n, d):
+    """Every row's score is the same whatever its position (exclusion == rebuild, shard-invariance)."""
+    rng = np.random.default_rng(n + d)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    w = rng.standard_normal(d)
+    s = otf.score_dense(w, x)
+    perm = rng.permutation(n)
+    np.testing.assert_array_equal(otf.score_dense(w, x[perm]), s[perm])
+    ex = exact_dense(x, w)
+    assert np.all(np.abs(s - ex) <= np.spacing(np.abs(s)) * 0.5 + 1e-12 * np.abs(ex) + 1e-30)
+
+
+def test_exclusion_equals_rebuild(otf):
+    """tests/test_ranker.py:253-266: without_ids ranks exactly like a rebuilt store."""
+    rng = np.random.default_rng(21)
+    data = rng.standard_normal((200, 16)).astype(np.float32)
+    names = [f"item-{i}" for i in range(200)]
+    store = otf.FeatureStore(data, names=names)
+    model = otf.LinearModel(rng.standard_normal(16), iteration=5, version=1)
+    excluded = {int(i) for i in rng.choice(200, size=40, replace=False)}
+    a = otf.Repository.dense(store).without_ids(excluded).rank(model, 25)
+    keep = [i for i in range(200) if i not in excluded]
+    b = otf.Repository.dense(store.subset(np.array(keep))).rank(model, 25)
+    assert list(a.ids) == list(b.ids)
+    np.testing.assert_array_equal(a.scores, b.scores)
+    assert a.names == b.names
+    r = otf.Repository.dense(store).without_ids({0, 1, 2})
+    assert r.count == 197 and int(r.ids.min()) == 3
+
+
+def test_repository_views(otf):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((120, 16)).astype(np.float32)
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    assert repo.payload_bytes() == 120 * 16 * 4 and repo.count == 120 and repo.model_dim == 16
+    vecs = rng.standard_normal((3, 16)).astype(np.float32)
+    np.testing.assert_array_equal(repo.adapt_training_vectors(vecs), vecs)
+    w = rng.standard_normal(16)
+    b = repo.rank(otf.LinearModel(w, 1), 10)
+    c = repo.rank(w, 10)  # a bare array is accepted as the model (ranker.py:59-60)
+    assert list(b.ids) == list(c.ids)  # repeated calls are bitwise identical
+    np.testing.assert_array_equal(b.scores, c.scores)
+
+
+# ---------------------------------------------------------------------------------------------
+# top_k (ranker.py:97-143)
+
+
+def test_top_k_known_answers(otf, golden):
+    r = otf.top_k(np.array([0.5, 2.0, -1.0, 2.0]), 10)
+    assert list(r.ids) == [1, 3, 0, 2]
+    np.testing.assert_array_equal(r.scores, [2.0, 2.0, 0.5, -1.0])
+    assert list(otf.top_k(np.ones(10), 4).ids) == [0, 1, 2, 3]
+    r = otf.top_k(golden["topk_ties_scores"], 100, ids=golden["topk_ties_ids_in"])
+    np.testing.assert_array_equal(r.ids, golden["topk_ties_ids"])
+    np.testing.assert_array_equal(r.scores, golden["topk_ties_out_scores"])
+    np.testing.assert_array_equal(otf.top_k(golden["topk_rand_scores"], 50).ids, golden["topk_rand_ids"])
+    np.testing.assert_array_equal(otf.top_k(golden["topk_signed_zero_scores"], 4).ids, golden["topk_signed_zero_ids"])
+    np.testing.assert_array_equal(otf.top_k(golden["topk_f64_scores"], 1000).ids, golden["topk_f64_ids"])
+    np.testing.assert_array_equal(otf.top_k(golden["topk_f64_scores"][:700], 5000).ids, golden["topk_full_ids"])
+    r = otf.top_k(np.array([1.0, 3.0, 2.0]), 2, ids=np.array([7, 8, 9]), names=["a", "b", "c"])
+    assert list(r.ids) == [8, 9] and r.names == ("b", "c")
+    assert len(otf.top_k(np.ones(5), 0)) == 0
+    with pytest.raises(otf.ConfigError):
+        otf.top_k(np.ones(5), 2, ids=np.arange(4))
+
+
+@pytest.mark.parametrize("n,k,dtype,kind", [
+    (1, 1, np.float32, "rand"), (5000, 4999, np.float32, "rand"), (100_000, 1000, np.float32, "rand"),
+    (100_000, 1000, np.float64, "rand"), (70_000, 5000, np.float32, "ties"), (50_000, 1000, np.float64, "ties"),
+    (20_000, 20_000, np.float32, "rand"), (9000, 4097, np.float64, "rand"), (3000, 1000, np.float32, "equal"),
+    (65_536, 300, np.float32, "neg"),
+])
+def test_top_k_matches_oracle(otf, n, k, dtype, kind):
+    rng = np.random.default_rng(n + k)
+    if kind == "rand":
+        s = rng.standard_normal(n).astype(dtype)
+    elif kind == "ties":
+        s = rng.integers(-4, 5, size=n).astype(dtype)
+    elif kind == "equal":
+        s = np.full(n, 0.25, dtype=dtype)
+    else:
+        s = -np.abs(rng.standard_normal(n)).astype(dtype)
+    ids = rng.permutation(n * 3)[:n].astype(np.int64)
+    r = otf.top_k(s, k, ids=ids)
+    o_ids, o_sc, _ = O.top_k(s, k, ids)
+    np.testing.assert_array_equal(r.ids, o_ids)
+    np.testing.assert_array_equal(r.scores, o_sc)
+
+
+def test_top_k_affine_invariance(otf):
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        s = rng.integers(0, 20, size=200).astype(np.float64)
+        scale, shift = rng.uniform(0.25, 8.0), rng.uniform(-5, 5)
+        assert list(otf.top_k(s, 25).ids) == list(otf.top_k(s * scale + shift, 25).ids)
+
+
+# ---------------------------------------------------------------------------------------------
+# PQ (pq.py:248-276) — bit-exact
+
+
+@pytest.mark.parametrize("name", PQ)
+def test_pq_bit_exact(otf, golden, name):
+    cents, codes, w = golden[f"pq_{name}_cents"], golden[f"pq_{name}_codes"], golden[f"pq_{name}_w"]
+    book = otf.PQCodebook(cents)
+    lut = otf.build_score_lut(w, book)
+    assert lut.tobytes() == golden[f"pq_{name}_lut"].tobytes()
+    s = otf.score_codes(golden[f"pq_{name}_lut"], codes)
+    assert s.tobytes() == golden[f"pq_{name}_scores"].tobytes()
+    np.testing.assert_array_equal(otf.score_pq(w, book, codes), s)
+    repo = otf.Repository.quantized(book, codes)
+    assert repo.score(w).tobytes() == golden[f"pq_{name}_scores"].tobytes()
+    r = repo.rank(otf.LinearModel(w, 1, 1), 40)
+    np.testing.assert_array_equal(r.ids, golden[f"pq_{name}_rank_ids"])
+    assert r.scores.tobytes() == golden[f"pq_{name}_rank_scores"].tobytes()
+    assert repo.payload_bytes() == codes.size and repo.model_dim == w.size
+
+
+def test_pq_errors(otf):
+    cents = np.random.default_rng(0).standard_normal((4, 8, 2)).astype(np.float32)
+    book = otf.PQCodebook(cents)
+    with pytest.raises(otf.ConfigError):
+        otf.build_score_lut(np.zeros(7), book)
+    with pytest.raises(otf.ConfigError):
+        otf.Repository.quantized(book, np.zeros((3, 5), np.uint8))
+    with pytest.raises(otf.CorruptionError):
+        otf.Repository.quantized(book, np.full((3, 4), 9, np.uint8))
+    lut = otf.build_score_lut(np.zeros(8), book)
+    assert lut.shape == (4, 8) and not np.any(lut)
+
+
+def test_pq_single_code_and_width_check(otf):
+    rng = np.random.default_rng(2)
+    lut = rng.standard_normal((16, 256))
+    codes = rng.integers(0, 256, (5, 16)).astype(np.uint8)
+    assert otf.score_codes(lut, codes[0]) == O.score_codes(lut, codes[:1])[0]
+    with pytest.raises(otf.ConfigError):
+        otf.score_codes(lut, codes[:, :15])
+
+
+# ---------------------------------------------------------------------------------------------
+# binary (ranker.py:78-94, binary.py:86-128)
+
+
+@pytest.mark.parametrize("name", BIN)
+def test_binary_parity(otf, golden, name):
+    bits = int(name[1:])
+    codes, w = golden[f"bin_{name}_codes"], golden[f"bin_{name}_w"]
+    ref = golden[f"bin_{name}_scores"].astype(np.float64)
+    tol = 1e-6 * np.linalg.norm(w) * np.sqrt(bits)
+    s = otf.score_binary(w, codes, bits)
+    assert s.dtype == np.float32
+    assert np.max(np.abs(s - ref)) <= tol
+    exact = O.unpack_bits(codes, bits).astype(np.float64) @ w.astype(np.float32).astype(np.float64)
+    assert np.all(np.abs(s - exact) <= np.spacing(np.abs(s)) * 0.5 + 1e-12 * np.abs(exact) + 1e-30)
+    np.testing.assert_array_equal(otf.unpack_bits(codes[:20], bits), golden[f"bin_{name}_unpacked"])
+    np.testing.assert_array_equal(otf.hamming_distance(codes, golden[f"bin_{name}_other"]), golden[f"bin_{name}_hamming"])
+    frame = golden.get(f"bin_{name}_frame")
+    m = frame.shape[1] if frame is not None else 128
+    codec = otf.BinaryCodec(otf.TightFrame(frame if frame is not None else np.eye(bits, m)), np.zeros(m, np.float32)
+                            if frame is None else golden[f"bin_{name}_center"])
+    repo = otf.Repository.binary(codec, codes)
+    np.testing.assert_array_equal(repo.score(w), s)
+    r = repo.rank(otf.LinearModel(w, 1, 2), 30)
+    o_ids, o_sc, _ = O.top_k(s, 30)
+    np.testing.assert_array_equal(r.ids, o_ids)
+    assert_rank_parity(r.ids, golden[f"bin_{name}_rank_ids"], dict(enumerate(ref)), tol)
+    if frame is not None:
+        got = otf.binarize(codec, golden[f"bin_{name}_vecs"])
+        np.testing.assert_array_equal(got, codes)
+        np.testing.assert_array_equal(repo.adapt_training_vectors(golden[f"bin_{name}_vecs"][:10]),
+                                      golden[f"bin_{name}_adapted"])
+
+
+def test_binary_edge_cases(otf):
+    w = np.random.default_rng(0).standard_normal(32)
+    np.testing.assert_array_equal(otf.score_binary(w, np.zeros((6, 4), np.uint8), 32), 0.0)
+    np.testing.assert_allclose(otf.score_binary(w, np.full((3, 4), 0xFF, np.uint8), 32), w.sum(), rtol=1e-5)
+    with pytest.raises(otf.ConfigError):
+        otf.score_binary(np.zeros(16), np.zeros((2, 4), np.uint8), 32)
+    packed = np.array([[0b00000001, 0b00000001]], dtype=np.uint8)
+    bits = otf.unpack_bits(packed, 9)
+    expected = np.zeros(9, np.float32)
+    expected[0] = expected[8] = 1.0
+    np.testing.assert_array_equal(bits[0], expected)
+    # padding bits are ignored when scoring (count=output_bits)
+    w13 = np.random.default_rng(1).standard_normal(13)
+    a = otf.score_binary(w13, np.array([[0xFF, 0x1F]], np.uint8), 13)
+    b = otf.score_binary(w13, np.array([[0xFF, 0xFF]], np.uint8), 13)
+    np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------------------------
+# Pegasos (trainer.py:51-173)
+
+
+def test_pegasos_known_answers(otf):
+    cfg = otf.TrainerConfig(lam=1.0, batch_size=2, seed=0)
+    w1 = otf.pegasos_step(np.zeros(2), 1, np.array([[1.0, 0.0]]), np.array([[0.0, 1.0]]), cfg, np.random.default_rng(0))
+    np.testing.assert_allclose(w1, [0.5, -0.5], rtol=1e-12)
+    w5 = otf.pegasos_step(np.array([2.0, 0.0]), 5, np.array([[1.1, 0.0]]), np.array([[-1.1, 0.0]]),
+                          otf.TrainerConfig(lam=0.04, batch_size=2), np.random.default_rng(0))
+    np.testing.assert_allclose(w5, [1.6, 0.0], rtol=1e-12)
+    w2 = otf.pegasos_step(np.array([1.0, 0.0]), 2, np.array([[0.5, 0.0]]), np.array([[-3.0, 0.0]]),
+                          otf.TrainerConfig(lam=0.25, batch_size=2), np.random.default_rng(0))
+    np.testing.assert_allclose(w2, [1.0, 0.0], rtol=1e-12)
+    capped = otf.pegasos_step(np.zeros(2), 1, np.array([[1.0, 0.0]]), np.array([[-1.0, 0.0]]),
+                              otf.TrainerConfig(lam=0.01, batch_size=2), np.random.default_rng(0))
+    np.testing.assert_allclose(np.linalg.norm(capped), 10.0, rtol=1e-12)
+    free = otf.pegasos_step(np.zeros(2), 1, np.array([[1.0, 0.0]]), np.array([[-1.0, 0.0]]),
+                            otf.TrainerConfig(lam=0.01, batch_size=2, project=False), np.random.default_rng(0))
+    np.testing.assert_allclose(np.linalg.norm(free), 100.0, rtol=1e-12)
+    with pytest.raises(otf.NotReadyError):
+        otf.pegasos_step(np.zeros(2), 1, np.empty((0, 2)), np.ones((1, 2)), cfg, np.random.default_rng(0))
+    with pytest.raises(otf.InsufficientDataError):
+        otf.pegasos_step(np.zeros(2), 1, np.ones((1, 2)), np.empty((0, 2)), cfg, np.random.default_rng(0))
+
+
+def test_pegasos_sequence_matches_reference(otf, golden):
+    pos, neg = golden["peg_pos"], golden["peg_neg"]
+    rng = np.random.default_rng(5)
+    w = np.zeros(pos.shape[1])
+    cfg = otf.TrainerConfig(lam=0.3, batch_size=8, project=False, seed=0)
+    for t in range(1, 31):
+        w = otf.pegasos_step(w, t, pos.astype(np.float64), neg.astype(np.float64), cfg, rng)
+        np.testing.assert_allclose(w, golden["peg_noproj_w"][t - 1], rtol=1e-12, atol=1e-15)
+
+
+def test_online_trainer_matches_reference(otf, golden):
+    pos, neg = golden["peg_pos"], golden["peg_neg"]
+    idx = []
+    tr = otf.OnlineTrainer(pos.shape[1], neg, otf.TrainerConfig(lam=0.05, batch_size=16, seed=9),
+                           batch_hook=lambda p, q: idx.append(np.concatenate([p, q])))
+    with pytest.raises(otf.NotReadyError):
+        tr.snapshot()
+    for t in range(60):
+        assert tr.step(pos) == t + 1
+        snap = tr.snapshot()
+        np.testing.assert_allclose(snap.weights, golden["peg_w"][t], rtol=1e-12, atol=1e-15)
+        assert snap.iteration == t + 1 and snap.version == t + 1
+    np.testing.assert_array_equal(np.stack(idx), golden["peg_idx"])
+    again = tr.snapshot()
+    assert again.version == 60
+    with pytest.raises(ValueError):
+        again.weights[0] = 1.0
+
+
+def test_online_trainer_device_pool_equals_host_pool(otf, golden):
+    pos, neg = golden["peg_pos"], golden["peg_neg"]
+    a = otf.OnlineTrainer(pos.shape[1], neg, otf.TrainerConfig(lam=0.05, batch_size=16, seed=9))
+    b = otf.OnlineTrainer(pos.shape[1], neg, otf.TrainerConfig(lam=0.05, batch_size=16, seed=9))
+    b.append_positives(pos[:10])
+    assert b.append_positives(pos[10:]) == len(pos)
+    for _ in range(40):
+        a.step(pos)
+        b.step()
+    np.testing.assert_array_equal(a.snapshot().weights, b.snapshot().weights)
