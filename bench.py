@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""bench.py — dataset images scored + exactly ranked per second on B200 (BASELINE.json metric).
+
+One "step" = one query of the on-the-fly ranker: w (float64, resident) -> score every row of the
+GPU-resident repository with the linear SVM -> exact top-k by (-score, id) -> (N>1: NCCL
+all_gather of the k local candidates + exact merge on the GPU). At N=1 the default workload is
+BASELINE.json configs[1] (C2: 1M x 2048-D float32 rows, top-1000); under torchrun every rank holds
+its own shard of that size (weak scaling, rows sharded by image, w broadcast from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4|c5a] [--impl reference]
+
+Rank 0 prints ONE JSON line. `value` is device-timed (CUDA events on the launching stream, max
+over ranks); `e2e` is the same metric through the public API (Repository.rank /
+ShardedRepository.rank with host w in, host RankedList out, copies inside the timed region);
+`roofline` is the dominant (scoring) kernel's algorithmic HBM bytes / its event-timed duration;
+`cpu_baseline` is the oracle port (numpy, the reference's own arithmetic) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L2_BYTES = 126 * 1024 * 1024
+
+CONFIGS = {
+    "c2": dict(kind="dense", rows=1_000_000, dim=2048, k=1000,
+               workload="C2: 1M x 2048-D fp32 features per GPU, single-query linear-SVM score + exact top-1000"),
+    "c1": dict(kind="dense", rows=1_000_000, dim=128, k=1000,
+               workload="C1: 1M x 128-D fp32 features per GPU, single-query linear-SVM score + exact top-1000"),
+    "c4": dict(kind="dense", rows=6_250_000, dim=2048, k=1000,
+               workload="C4: 6.25M x 2048-D fp32 rows per GPU (50M over 8 GPUs), score + top-1000 + NCCL merge"),
+    "c3": dict(kind="pq", rows=10_000_000, dim=16, k=1000, subdim=8,
+               workload="C3: 10M PQ codes per GPU (16 sub-quantizers x 256 centroids, 128-D), LUT score + top-1000"),
+    "c5a": dict(kind="binary", rows=100_000_000, dim=2048, k=1000,
+                workload="C5a: 100M x 2048-bit packed binary codes per GPU, score + top-1000"),
+}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def row_bytes(cfg) -> int:
+    if cfg["kind"] == "dense":
+        return 4 * cfg["dim"]
+    if cfg["kind"] == "pq":
+        return cfg["dim"]
+    return cfg["dim"] // 8
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port (numpy = the reference's own arithmetic)
+
+
+def cpu_sample(cfg, seed=1234):
+    """A bounded host sample of the workload and its oracle ranker (sized to ~0.05-0.2 s/query)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import otf_oracle as O
+
+    rng = np.random.default_rng(seed)
+    kind, dim, k = cfg["kind"], cfg["dim"], cfg["k"]
+    if kind == "dense":
+        rows = max(20_000, min(cfg["rows"], (1 << 30) // (4 * dim)))  # <= 1 GiB of features
+        x = rng.standard_normal((rows, dim), dtype=np.float32)
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        w = rng.standard_normal(dim)
+        fn = lambda: O.top_k(O.score_dense(w, x), k)
+        desc = f"{rows} x {dim}-D fp32 rows (score_dense + top_k, ranker.py:63-143)"
+    elif kind == "pq":
+        rows = min(cfg["rows"], 2_000_000)
+        cents = rng.standard_normal((dim, 256, cfg["subdim"])).astype(np.float32)
+        codes = rng.integers(0, 256, (rows, dim), dtype=np.uint8)
+        w = rng.standard_normal(dim * cfg["subdim"])
+        fn = lambda: O.top_k(O.score_pq(w, cents, codes), k)
+        desc = f"{rows} PQ codes x {dim} blocks (build_score_lut + score_codes + top_k, pq.py:248-276)"
+    else:
+        rows = min(cfg["rows"], 100_000)
+        codes = rng.integers(0, 256, (rows, dim // 8), dtype=np.uint8)
+        w = rng.standard_normal(dim)
+        fn = lambda: O.top_k(O.score_binary(w, codes, dim), k)
+        desc = f"{rows} x {dim}-bit codes (score_binary + top_k, ranker.py:78-143)"
+    return rows, fn, desc
+
+
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+        if n and n[0]:
+            return int(n[0])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    rows, fn, desc = cpu_sample(cfg)
+    for _ in range(max(args.warmup, 1)):
+        fn()
+    times = []
+    t_end = time.perf_counter() + 240.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    per = float(np.mean(times))
+    value = rows / per
+    line = {
+        "impl": "reference", "metric": "dataset images scored+ranked/sec", "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["kind"] != "pq" else "f64",
+        "data": "synthetic", "config": {"workload": cfg["workload"], "k": cfg["k"], "sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cpu_threads(), "kind": "port",
+                         "sample": desc + " on host cores; the reference itself (pure numpy) cannot travel to the GPU box"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU arm
+
+
+def make_repository(cfg, rank, world, device, seed=20260418):
+    import torch
+
+    import paper_1407_4764_b200 as otf
+
+    dev = torch.device("cuda", device)
+    n = cfg["rows"]
+    start = rank * n  # weak scaling: every rank holds its own n rows; global ids are disjoint
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + 7919 * rank)
+    keep = {}
+    if cfg["kind"] == "dense":
+        d = cfg["dim"]
+        x = torch.empty((n, d), dtype=torch.float32, device=dev)
+        chunk = max(1, (1 << 28) // d)
+        for s in range(0, n, chunk):
+            v = x[s:s + chunk]
+            v.normal_(generator=g)
+            v /= v.norm(dim=1, keepdim=True)
+        keep["x"] = x
+        repo = otf.Repository.from_device("dense", x.data_ptr(), n, d, id_base=start)
+    elif cfg["kind"] == "pq":
+        m, q = cfg["dim"], cfg["subdim"]
+        codes = torch.randint(0, 256, (n, m), dtype=torch.uint8, device=dev, generator=g)
+        cents = np.random.default_rng(seed).standard_normal((m, 256, q)).astype(np.float32)
+        keep["codes"] = codes
+        repo = otf.Repository.from_device("pq", codes.data_ptr(), n, m, id_base=start,
+                                          codebook=otf.PQCodebook(cents))
+    else:
+        bits = cfg["dim"]
+        codes = torch.empty((n, bits // 8), dtype=torch.uint8, device=dev)
+        chunk = 1 << 24
+        for s in range(0, n, chunk):
+            codes[s:s + chunk].random_(0, 256, generator=g)
+        keep["codes"] = codes
+        repo = otf.Repository.from_device("binary", codes.data_ptr(), n, bits, id_base=start)
+    torch.cuda.synchronize(dev)
+    return repo, keep, start
+
+
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1407_4764_b200 as otf
+    from paper_1407_4764_b200 import _lib
+    from paper_1407_4764_b200.distributed import ShardedRepository
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    otf.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    repo, keep, start = make_repository(cfg, rank, world, local)
+    n_local = repo.count
+    k = cfg["k"]
+    total_rows = n_local * world
+    dim = repo.model_dim
+    w = np.random.default_rng(99).standard_normal(dim)
+    w_dev = torch.as_tensor(w, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    lib = _lib.load()
+
+    if world > 1:
+        sharded = ShardedRepository.from_local(repo, total_rows, start)
+        step = lambda: sharded.rank_device(w_dev, k)
+    else:
+        o_ids = torch.empty(k, dtype=torch.int64, device=dev)
+        o_sc = torch.empty(k, dtype=torch.float64, device=dev)
+        o_rows = torch.empty(k, dtype=torch.int64, device=dev)
+        got = C.c_int64()
+
+        def step():
+            _lib.check(lib.otf_repo_rank(repo.handle, _lib.tptr(w_dev), k, _lib.tptr(o_ids), _lib.tptr(o_sc),
+                                         _lib.tptr(o_rows), C.byref(got), _lib.MEM_DEVICE, sp))
+
+    payload = n_local * row_bytes(cfg)
+    flush = payload < 4 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed region: K steps, per-step CUDA events on the launching stream ----------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush:
+                scratch.add_(1.0)  # evict the repository from L2 between timed steps (not timed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = _lib.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = float(np.sum(step_ms)) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    value = total_rows / (ms / 1e3)
+
+    # ---- dominant kernel (scoring) alone, event-timed: roofline ---------------------------
+    score_buf = torch.empty(n_local, dtype=torch.float64 if cfg["kind"] == "pq" else torch.float32, device=dev)
+    reps = max(5, min(50, args.steps))
+    ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kms = []
+    for _ in range(reps):
+        if flush:
+            scratch.add_(1.0)
+        ks.record(stream)
+        _lib.check(lib.otf_repo_score(repo.handle, _lib.tptr(w_dev), _lib.tptr(score_buf), _lib.MEM_DEVICE, sp))
+        ke.record(stream)
+        torch.cuda.synchronize(dev)
+        kms.append(ks.elapsed_time(ke))
+    kern_ms = float(np.mean(kms))
+    peak, peak_src = load_peaks()
+    achieved = payload / (kern_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API (host w in, host RankedList out) ---------------
+    e2e_steps = max(3, min(args.steps, 200))
+    model = otf.LinearModel(w, 1, 1)
+    if world > 1:
+        api = lambda: sharded.rank(model, k, root_only=True)
+    else:
+        api = lambda: repo.rank(model, k)
+    for _ in range(3):
+        api()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e2e_t = []
+    for _ in range(e2e_steps):
+        if flush:
+            scratch.add_(1.0)
+            torch.cuda.synchronize(dev)
+        barrier()
+        t0 = time.perf_counter()
+        api()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = total_rows / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rows, fn, desc = cpu_sample(cfg)
+        fn()
+        tt = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            tt.append(time.perf_counter() - t0)
+        cpu = {"value": rows / min(tt), "unit": "images/s", "cores": cpu_threads(), "kind": "port",
+               "sample": desc + ", oracle port (numpy) best of 3 on this host"}
+
+    if rank == 0:
+        line = {
+            "metric": "dataset images scored+ranked/sec",
+            "value": value,
+            "unit": "images/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"dense": "f32 (f64 accumulate)", "pq": "f64", "binary": "f32 (f64 accumulate)"}[cfg["kind"]],
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "rows_per_gpu": n_local, "total_rows": total_rows,
+                       "dim_or_blocks_or_bits": cfg["dim"], "k": k, "parallelism": f"dp{world} (rows sharded)",
+                       "l2": ("L2 flushed between timed steps" if flush else
+                              f"inputs ({payload / 1e9:.1f} GB/GPU) larger than L2")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"{cfg['kind']} score (otf_repo_score: scan of {payload / 1e9:.3f} GB)",
+                         "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": dim * 8,
+                    "d2h_bytes_per_step": k * 24, "ms_per_query": e2e_s * 1e3},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = 20 if args.impl == "reference" else 500
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -15,7 +15,7 @@
  *   - `mem` arguments say where caller pointers live: OTF_MEM_HOST (pageable or pinned host
  *     memory; the call is synchronous and copies in/out) or OTF_MEM_DEVICE (device pointers on
  *     the handle's device; the call is asynchronous on `stream`, a cudaStream_t passed as
- *     void*, NULL = the handle's own stream).
+ *     void*; NULL is the legacy default stream, as everywhere in CUDA).
  *   - Scores are computed with the semantics of the reference: dense/binary scores are
  *     float32 of <x, float32(w)> (ranker.py:69, :89-93), PQ scores are float64 of the
  *     float64 LUT sum (pq.py:248-276). Ranked lists order by (-score, id) with ties toward

@@ -21,37 +21,39 @@ namespace otf {
 // group owns chunks {l + 16*t}. Nibble i (0..31) of chunk c has value v; its table entry
 // T[c][i][v] is stored at double index ((t*32 + i)*16 + v)*16 + (c % 16), with t = c/16,
 // so the 16 lanes of a half-warp always hit 16 distinct bank pairs.
-__global__ void bin_build_nibble_lut(const double* __restrict__ w, int n_bits,
-                                     int chunks, double* __restrict__ lut) {
-  const int total = chunks * 32 * 16;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int v = e & 15;
-    const int i = (e >> 4) & 31;
-    const int c = e >> 9;
-    const int bit0 = c * 128 + i * 4;
-    double s = 0.0;
+__device__ __forceinline__ double nibble_entry(const double* __restrict__ w, int n_bits, int e,
+                                               int* slot) {
+  const int v = e & 15;
+  const int i = (e >> 4) & 31;
+  const int c = e >> 9;
+  const int bit0 = c * 128 + i * 4;
+  double s = 0.0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int j = bit0 + b;
-      if ((v >> b) & 1) {
-        const double wj = j < n_bits ? (double)__double2float_rn(w[j]) : 0.0;
-        s = __dadd_rn(s, wj);
-      }
-    }
-    const int t = c >> 4, lane = c & 15;
-    lut[((t * 32 + i) * 16 + v) * 16 + lane] = s;
+  for (int b = 0; b < 4; ++b) {
+    const int j = bit0 + b;
+    if ((v >> b) & 1) s = __dadd_rn(s, j < n_bits ? (double)__double2float_rn(w[j]) : 0.0);
   }
+  const int t = c >> 4, lane = c & 15;
+  *slot = ((t * 32 + i) * 16 + v) * 16 + lane;
+  return s;
 }
 
 // Fast path: row bytes == 16 * CH (CH chunks of 16 bytes, CH % 16 == 0), R rows per group
-// per iteration; 2 groups (half-warps) per warp.
+// per iteration; 2 groups (half-warps) per warp. The nibble tables are built per CTA from w.
 template <int CH, int R>
 __global__ void __launch_bounds__(256) bin_score_fast(const uint8_t* __restrict__ codes, int64_t n,
-                                                      const double* __restrict__ lut_g,
-                                                      float* __restrict__ out) {
+                                                      const double* __restrict__ w, int n_bits,
+                                                      float* __restrict__ out,
+                                                      uint32_t* __restrict__ ghist) {
   constexpr int TPL = CH / 16;  // chunks per lane
   extern __shared__ double lut[];  // CH*32*16 doubles
-  for (int t = threadIdx.x; t < CH * 32 * 16; t += blockDim.x) lut[t] = lut_g[t];
+  __shared__ uint32_t sh[kHistBins];
+  for (int e = threadIdx.x; e < CH * 32 * 16; e += blockDim.x) {
+    int slot;
+    const double v = nibble_entry(w, n_bits, e, &slot);
+    lut[slot] = v;
+  }
+  if (ghist) hist_zero(sh);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int cl = lane & 15;    // chunk lane
@@ -89,16 +91,27 @@ __global__ void __launch_bounds__(256) bin_score_fast(const uint8_t* __restrict_
     bool writer;
     const int slot = row_of_lane<R, 16>(lane, &writer);
     const int64_t row = r0 + grp * R + slot;
-    if (writer && row < n) out[row] = __double2float_rn(p[0]);
+    const bool active = writer && row < n;
+    const float s = __double2float_rn(p[0]);
+    if (active) out[row] = s;
+    if (ghist) hist_add(sh, active, hist_bin(s));
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
   }
 }
 
-// Generic path: any n_bits. One warp per row; lane l owns bytes {l + 32*t}, low nibble
-// then high nibble; weights read from a float32 copy of w in global memory.
+// Generic path: any n_bits. One warp per row; lane l owns bytes {l + 32*t}, bits in order;
+// float32(w_j) converted on the fly.
 __global__ void __launch_bounds__(256) bin_score_generic(const uint8_t* __restrict__ codes, int64_t n,
                                                          int n_bits, int row_bytes,
-                                                         const float* __restrict__ w32,
-                                                         float* __restrict__ out) {
+                                                         const double* __restrict__ w,
+                                                         float* __restrict__ out,
+                                                         uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kHistBins];
+  if (ghist) hist_zero(sh);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -110,12 +123,18 @@ __global__ void __launch_bounds__(256) bin_score_generic(const uint8_t* __restri
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int j = 8 * b + q;
-        if (((byte >> q) & 1u) && j < n_bits) acc = __dadd_rn(acc, (double)w32[j]);
+        if (((byte >> q) & 1u) && j < n_bits) acc = __dadd_rn(acc, (double)__double2float_rn(w[j]));
       }
     }
     double p[1] = {acc};
     transposed_reduce<1, 32>(p, lane);
-    if (lane == 0) out[row] = __double2float_rn(p[0]);
+    const float s = __double2float_rn(p[0]);
+    if (lane == 0) out[row] = s;
+    if (ghist) hist_add(sh, lane == 0, hist_bin(s));
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
   }
 }
 
@@ -178,17 +197,9 @@ size_t bin_lut_bytes(int n_bits) {
   return (size_t)(row_bytes / 16) * 32 * 16 * sizeof(double);
 }
 
-int launch_bin_lut(const double* w, int n_bits, double* lut, cudaStream_t st) {
-  const int chunks = ((n_bits + 7) / 8) / 16;
-  const int total = chunks * 32 * 16;
-  bin_build_nibble_lut<<<(total + 255) / 256, 256, 0, st>>>(w, n_bits, chunks, lut);
-  OTF_LAUNCH_CHECK("bin_build_nibble_lut");
-  return OTF_OK;
-}
-
 template <int CH, int R>
-static int launch_fast(const uint8_t* codes, int64_t n, const double* lut, float* out, int device,
-                       cudaStream_t st) {
+static int launch_fast(const uint8_t* codes, int64_t n, const double* w, int n_bits, float* out,
+                       uint32_t* hist, int device, cudaStream_t st) {
   auto fn = bin_score_fast<CH, R>;
   const size_t smem = (size_t)CH * 32 * 16 * sizeof(double);
   static bool configured[64] = {false};
@@ -202,25 +213,25 @@ static int launch_fast(const uint8_t* codes, int64_t n, const double* lut, float
   int64_t grid = (int64_t)per_sm * sm_count(device);
   const int64_t need = (n + 16 * R - 1) / (16 * R);
   if (need < grid) grid = need;
-  fn<<<(int)grid, 256, smem, st>>>(codes, n, lut, out);
+  fn<<<(int)grid, 256, smem, st>>>(codes, n, w, n_bits, out, hist);
   OTF_LAUNCH_CHECK("bin_score_fast");
   return OTF_OK;
 }
 
-// lut: from launch_bin_lut when bin_lut_bytes(n_bits) > 0; w32: float32 w for the generic path.
-int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* lut,
-                     const float* w32, float* out, int device, cudaStream_t st) {
+// w: float64 model (device); cast to float32 in-kernel (ranker.py:89). hist: see dense.
+int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
+                     uint32_t* hist, int device, cudaStream_t st) {
   if (n <= 0) return OTF_OK;
   const int row_bytes = (n_bits + 7) / 8;
   const bool aligned = (((uintptr_t)codes) & 15) == 0;
-  if (aligned && bin_lut_bytes(n_bits) > 0 && lut != nullptr) {
-    if (row_bytes == 256) return launch_fast<16, 8>(codes, n, lut, out, device, st);
-    if (row_bytes == 512) return launch_fast<32, 4>(codes, n, lut, out, device, st);
+  if (aligned && bin_lut_bytes(n_bits) > 0) {
+    if (row_bytes == 256) return launch_fast<16, 8>(codes, n, w, n_bits, out, hist, device, st);
+    if (row_bytes == 512) return launch_fast<32, 4>(codes, n, w, n_bits, out, hist, device, st);
   }
   int64_t grid = (n + 7) / 8;
   const int64_t cap = 8LL * sm_count(device);
   if (grid > cap) grid = cap;
-  bin_score_generic<<<(int)grid, 256, 0, st>>>(codes, n, n_bits, row_bytes, w32, out);
+  bin_score_generic<<<(int)grid, 256, 0, st>>>(codes, n, n_bits, row_bytes, w, out, hist);
   OTF_LAUNCH_CHECK("bin_score_generic");
   return OTF_OK;
 }

@@ -138,7 +138,8 @@ struct otf_trainer {
 namespace {
 
 cudaStream_t pick_stream(cudaStream_t own, void* user) {
-  return user ? static_cast<cudaStream_t>(user) : own;
+  (void)own;  // device-memory calls run on the caller's stream (NULL = legacy default stream)
+  return static_cast<cudaStream_t>(user);
 }
 
 int make_stream(cudaStream_t* s, bool high_priority) {
@@ -225,50 +226,39 @@ int stage_w(otf_repo* r, const double* w, int mem, cudaStream_t st, const double
   return OTF_OK;
 }
 
-// Scores every row of r into `out` (device); returns dtype of the scores.
-int score_into(otf_repo* r, const double* dw, void* out, cudaStream_t st) {
+// Scores every row of r into `out` (device). hist (nullable) receives the coarse histogram.
+int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStream_t st) {
   int rc = OTF_OK;
-  if (r->kind == OTF_KIND_DENSE) {
-    if ((rc = r->w32.ensure((size_t)r->model_dim * sizeof(float)))) return rc;
-    if ((rc = launch_cast_w(dw, static_cast<float*>(r->w32.p), r->model_dim, st))) return rc;
-    return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim,
-                              static_cast<const float*>(r->w32.p), static_cast<float*>(out),
-                              r->device, st);
-  }
+  if (r->kind == OTF_KIND_DENSE)
+    return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dw,
+                              static_cast<float*>(out), hist, r->device, st);
   if (r->kind == OTF_KIND_PQ) {
-    if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
-    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
-      return rc;
-    return launch_pq_scan(static_cast<const uint8_t*>(r->payload), r->n, r->M,
-                          static_cast<const double*>(r->lut.p), r->K, static_cast<double*>(out),
-                          r->device, st);
+    const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
+    if (!pq_fast_path(r->M, codes)) {  // generic path reads a separately built LUT
+      if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
+      if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
+        return rc;
+    }
+    return launch_pq_scan(codes, r->n, r->M, r->cents, dw, static_cast<const double*>(r->lut.p), r->K,
+                          r->Q, static_cast<double*>(out), hist, r->device, st);
   }
-  // binary
-  const size_t lb = bin_lut_bytes(r->model_dim);
-  if (lb > 0) {
-    if ((rc = r->lut.ensure(lb))) return rc;
-    if ((rc = launch_bin_lut(dw, r->model_dim, static_cast<double*>(r->lut.p), st))) return rc;
-    return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim,
-                            static_cast<const double*>(r->lut.p), nullptr,
-                            static_cast<float*>(out), r->device, st);
-  }
-  if ((rc = r->w32.ensure((size_t)r->model_dim * sizeof(float)))) return rc;
-  if ((rc = launch_cast_w(dw, static_cast<float*>(r->w32.p), r->model_dim, st))) return rc;
-  return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, nullptr,
-                          static_cast<const float*>(r->w32.p), static_cast<float*>(out),
-                          r->device, st);
+  return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, dw,
+                          static_cast<float*>(out), hist, r->device, st);
 }
 
 int score_dtype(const otf_repo* r) { return r->kind == OTF_KIND_PQ ? OTF_F64 : OTF_F32; }
 
+// One query on device: scoring kernel (+ fused histogram) then the top-k kernel.
 int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, double* scores,
                 int64_t* rows, cudaStream_t st) {
   const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
   int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
   if (rc) return rc;
-  if ((rc = score_into(r, dw, r->scores.p, st))) return rc;
-  return launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, ids,
-                     scores, rows, r->device, st);
+  if ((rc = topk_ws_alloc(&r->topk, k_eff))) return rc;
+  const bool fuse = k_eff < r->n;
+  if ((rc = score_into(r, dw, r->scores.p, fuse ? r->topk.hist : nullptr, st))) return rc;
+  return launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, fuse,
+                     ids, scores, rows, r->device, st);
 }
 
 }  // namespace
@@ -280,8 +270,8 @@ int otf_abi_version(void) { return 1; }
 int64_t otf_launch_count(void) { return g_launches.load(); }
 
 const char* otf_kernel_names(void) {
-  return "dense_score_fast;dense_score_generic;cast_w_f32;pq_build_lut_kernel;pq_scan_fast;"
-         "pq_scan_generic;pq_check_codes;bin_build_nibble_lut;bin_score_fast;bin_score_generic;"
+  return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;"
+         "pq_scan_generic;pq_check_codes;bin_score_fast;bin_score_generic;"
          "bin_unpack;bin_binarize;bin_hamming;topk_coop_kernel;pegasos_kernel;gather_rows_kernel;"
          "gather_i64_kernel";
 }
@@ -434,9 +424,9 @@ int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* strea
   int rc = stage_w(r, w, mem, st, &dw);
   if (rc) return rc;
   const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
-  if (mem == OTF_MEM_DEVICE) return score_into(r, dw, out, st);
+  if (mem == OTF_MEM_DEVICE) return score_into(r, dw, out, nullptr, st);
   if ((rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es))) return rc;
-  if ((rc = score_into(r, dw, r->scores.p, st))) return rc;
+  if ((rc = score_into(r, dw, r->scores.p, nullptr, st))) return rc;
   OTF_CUDA(cudaMemcpyAsync(out, r->scores.p, (size_t)r->n * es, cudaMemcpyDeviceToHost, st));
   OTF_CUDA(cudaStreamSynchronize(st));
   return OTF_OK;
@@ -565,18 +555,13 @@ int otf_score_dense(int device, const float* X, int64_t n, int32_t dim, const do
                     int mem, void* stream) {
   if (dim <= 0) return fail(OTF_ERR_CONFIG, "dim must be positive");
   STATELESS_BEGIN(device, mem, stream)
-  const void *dX, *dw; void* dout; DevBuf w32;
+  const void *dX, *dw; void* dout;
   if ((rc = S.in(X, (size_t)n * dim * 4, mem, &dX))) return rc;
   if ((rc = S.in(w, (size_t)dim * 8, mem, &dw))) return rc;
   if ((rc = S.outbuf(out, (size_t)n * 4, mem, &dout))) return rc;
-  if ((rc = w32.ensure((size_t)dim * 4))) return rc;
-  if ((rc = launch_cast_w(static_cast<const double*>(dw), static_cast<float*>(w32.p), dim, st))) return rc;
-  if ((rc = launch_dense_score(static_cast<const float*>(dX), n, dim, static_cast<const float*>(w32.p),
-                               static_cast<float*>(dout), device, st))) return rc;
-  rc = S.out(out, dout, (size_t)n * 4, mem);
-  if (mem == OTF_MEM_DEVICE) cudaStreamSynchronize(st);  // w32 is freed on return
-  w32.release();
-  return rc;
+  if ((rc = launch_dense_score(static_cast<const float*>(dX), n, dim, static_cast<const double*>(dw),
+                               static_cast<float*>(dout), nullptr, device, st))) return rc;
+  return S.out(out, dout, (size_t)n * 4, mem);
 }
 
 int otf_pq_build_lut(int device, const float* centroids, int32_t M, int32_t K, int32_t Q,
@@ -611,8 +596,9 @@ int otf_pq_score_codes(int device, const double* lut, int32_t M, int32_t K, cons
     bad.release();
     if (hb) return fail(OTF_ERR_CORRUPTION, "code value out of range for " + std::to_string(K) + " centroids");
   }
-  if ((rc = launch_pq_scan(static_cast<const uint8_t*>(dc), n, M, static_cast<const double*>(dl), K,
-                           static_cast<double*>(dout), device, st))) return rc;
+  if ((rc = launch_pq_scan(static_cast<const uint8_t*>(dc), n, M, nullptr, nullptr,
+                           static_cast<const double*>(dl), K, 0, static_cast<double*>(dout), nullptr,
+                           device, st))) return rc;
   return S.out(out, dout, (size_t)n * 8, mem);
 }
 
@@ -621,27 +607,13 @@ int otf_score_binary(int device, const uint8_t* codes, int64_t n, int32_t output
   if (output_bits <= 0) return fail(OTF_ERR_CONFIG, "output_bits must be positive");
   STATELESS_BEGIN(device, mem, stream)
   const int row_bytes = (output_bits + 7) / 8;
-  const void *dc, *dw; void* dout; DevBuf aux;
+  const void *dc, *dw; void* dout;
   if ((rc = S.in(codes, (size_t)n * row_bytes, mem, &dc))) return rc;
   if ((rc = S.in(w, (size_t)output_bits * 8, mem, &dw))) return rc;
   if ((rc = S.outbuf(out, (size_t)n * 4, mem, &dout))) return rc;
-  const size_t lb = bin_lut_bytes(output_bits);
-  if (lb) {
-    if ((rc = aux.ensure(lb))) return rc;
-    if ((rc = launch_bin_lut(static_cast<const double*>(dw), output_bits, static_cast<double*>(aux.p), st))) return rc;
-    rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<const double*>(aux.p),
-                          nullptr, static_cast<float*>(dout), device, st);
-  } else {
-    if ((rc = aux.ensure((size_t)output_bits * 4))) return rc;
-    if ((rc = launch_cast_w(static_cast<const double*>(dw), static_cast<float*>(aux.p), output_bits, st))) return rc;
-    rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, nullptr,
-                          static_cast<const float*>(aux.p), static_cast<float*>(dout), device, st);
-  }
-  if (rc) return rc;
-  rc = S.out(out, dout, (size_t)n * 4, mem);
-  if (mem == OTF_MEM_DEVICE) cudaStreamSynchronize(st);
-  aux.release();
-  return rc;
+  if ((rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<const double*>(dw),
+                             static_cast<float*>(dout), nullptr, device, st))) return rc;
+  return S.out(out, dout, (size_t)n * 4, mem);
 }
 
 int otf_unpack_bits(int device, const uint8_t* codes, int64_t n, int32_t output_bits, float* out,
@@ -702,7 +674,7 @@ int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const in
   if ((rc = S.outbuf(out_ids, (size_t)k_eff * 8, mem, &d_ids))) return rc;
   if ((rc = S.outbuf(out_scores, (size_t)k_eff * 8, mem, &d_sc))) return rc;
   if (out_rows && (rc = S.outbuf(out_rows, (size_t)k_eff * 8, mem, &d_rows))) return rc;
-  rc = launch_topk(ds, dtype, n, static_cast<const int64_t*>(di), 0, k_eff, &ws,
+  rc = launch_topk(ds, dtype, n, static_cast<const int64_t*>(di), 0, k_eff, &ws, false,
                    static_cast<int64_t*>(d_ids), static_cast<double*>(d_sc),
                    static_cast<int64_t*>(d_rows), device, st);
   if (!rc) rc = S.out(out_ids, d_ids, (size_t)k_eff * 8, mem);

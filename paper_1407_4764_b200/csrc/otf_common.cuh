@@ -49,6 +49,31 @@ template <typename T> struct KeyBits;
 template <> struct KeyBits<float> { static constexpr int value = 32; };
 template <> struct KeyBits<double> { static constexpr int value = 64; };
 
+// ---- coarse score histogram fused into the scoring kernels ---------------------------------
+// 4096 bins = the top 12 bits of the float32 order key (sign, 8 exponent bits, 3 mantissa
+// bits). float64 scores are bucketed through their float32 rounding, which is monotone, so a
+// bin ordering is always consistent with the exact score ordering. The top-k kernel uses the
+// histogram to find the bin that holds the k-th best entry without another pass over N.
+constexpr int kHistBins = 4096;
+__device__ __forceinline__ uint32_t hist_bin(float s) { return (uint32_t)(score_key(s) >> 20); }
+__device__ __forceinline__ uint32_t hist_bin(double s) { return hist_bin(__double2float_rn(s)); }
+
+__device__ __forceinline__ void hist_zero(uint32_t* sh) {
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0u;
+}
+// Warp-aggregated shared-memory histogram update; must be called by all 32 lanes.
+__device__ __forceinline__ void hist_add(uint32_t* sh, bool active, uint32_t bin) {
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  if (act == 0u) return;
+  const unsigned peers = __match_any_sync(0xffffffffu, active ? bin : 0xffffffffu);
+  const int lane = threadIdx.x & 31;
+  if (active && lane == __ffs(peers) - 1) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+}
+__device__ __forceinline__ void hist_flush(const uint32_t* sh, uint32_t* g) {
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
+    if (sh[b]) atomicAdd(&g[b], sh[b]);
+}
+
 // Streaming 128-bit load that does not allocate in L1 (the dataset is read once per query).
 __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   float4 r;

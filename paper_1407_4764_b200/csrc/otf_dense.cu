@@ -13,6 +13,10 @@
 // float64 partial; the 32 partials are then combined by the xor-butterfly tree
 // (l, l^16), (l, l^8), ..., (l, l^1).
 //
+// The float64 -> float32 cast of w (ranker.py:69) happens while w is staged into shared
+// memory, and the kernel also builds the coarse score histogram the top-k kernel starts from
+// (otf_common.cuh, hist_*), so one query = this kernel + the top-k kernel.
+//
 // HBM roofline: 4*d bytes per row; 0.5 flop/byte. Loads are 128-bit, coalesced, streamed
 // past L1 (ld.global.nc.L1::no_allocate); the grid is persistent (a multiple of the 148 SMs).
 #include "otf_common.cuh"
@@ -20,16 +24,20 @@
 
 namespace otf {
 
-// Fast path: d == 128 * CPL. Each warp handles R rows per iteration (R*CPL <= 16 float4
-// loads in flight per lane), then a transposed butterfly gives ~2 shuffles per row.
+// Fast path: d == 128 * CPL. Each warp handles R rows per iteration, then a transposed
+// butterfly gives ~2 shuffles per row.
 template <int CPL, int R>
 __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restrict__ X, int64_t n,
-                                                           const float* __restrict__ w32,
-                                                           float* __restrict__ out) {
+                                                           const double* __restrict__ w,
+                                                           float* __restrict__ out,
+                                                           uint32_t* __restrict__ ghist) {
   const int lane = threadIdx.x & 31;
-  // w (float32) staged once per CTA in shared memory; lanes read consecutive float4s
   __shared__ float4 wr[32 * CPL];
-  for (int t = threadIdx.x; t < 32 * CPL; t += blockDim.x) wr[t] = reinterpret_cast<const float4*>(w32)[t];
+  __shared__ uint32_t sh[kHistBins];
+  for (int t = threadIdx.x; t < 32 * CPL; t += blockDim.x)
+    wr[t] = make_float4(__double2float_rn(w[4 * t]), __double2float_rn(w[4 * t + 1]),
+                        __double2float_rn(w[4 * t + 2]), __double2float_rn(w[4 * t + 3]));
+  if (ghist) hist_zero(sh);
   __syncthreads();
   const int64_t row_f4 = 32 * CPL;  // float4 per row
   const float4* X4 = reinterpret_cast<const float4*>(X);
@@ -70,14 +78,25 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
     bool writer;
     const int slot = row_of_lane<R, 32>(lane, &writer);
     const int64_t row = r0 + slot;
-    if (writer && row < n) out[row] = __double2float_rn(p[0]);
+    const bool active = writer && row < n;
+    const float s = __double2float_rn(p[0]);
+    if (active) out[row] = s;
+    if (ghist) hist_add(sh, active, hist_bin(s));
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
   }
 }
 
 // Generic path: any d (and any alignment). One warp per row, same canonical order.
 __global__ void __launch_bounds__(256) dense_score_generic(const float* __restrict__ X, int64_t n,
-                                                           int32_t d, const float* __restrict__ w32,
-                                                           float* __restrict__ out) {
+                                                           int32_t d, const double* __restrict__ w,
+                                                           float* __restrict__ out,
+                                                           uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kHistBins];
+  if (ghist) hist_zero(sh);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -88,19 +107,19 @@ __global__ void __launch_bounds__(256) dense_score_generic(const float* __restri
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = base + e;
-        if (j < d) acc = __fma_rn((double)__ldg(x + j), (double)w32[j], acc);
+        if (j < d) acc = __fma_rn((double)__ldg(x + j), (double)__double2float_rn(w[j]), acc);
       }
     }
     double p[1] = {acc};
     transposed_reduce<1, 32>(p, lane);
-    if (lane == 0) out[row] = __double2float_rn(p[0]);
+    const float s = __double2float_rn(p[0]);
+    if (lane == 0) out[row] = s;
+    if (ghist) hist_add(sh, lane == 0, hist_bin(s));
   }
-}
-
-// w (float64) -> float32 round-to-nearest (ranker.py:69 `w.astype(np.float32)`).
-__global__ void cast_w_f32(const double* __restrict__ w, float* __restrict__ w32, int32_t d) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
-    w32[j] = __double2float_rn(w[j]);
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
+  }
 }
 
 static int grid_for(const void* fn, int threads, int device) {
@@ -111,44 +130,39 @@ static int grid_for(const void* fn, int threads, int device) {
 }
 
 template <int CPL, int R>
-static int launch_fast(const float* X, int64_t n, const float* w32, float* out, int device,
-                       cudaStream_t st) {
+static int launch_fast(const float* X, int64_t n, const double* w, float* out, uint32_t* hist,
+                       int device, cudaStream_t st) {
   auto fn = dense_score_fast<CPL, R>;
   int grid = grid_for((const void*)fn, 256, device);
   const int64_t need = (n + (8 * R) - 1) / (8 * R);  // 8 warps per block
   if (need < grid) grid = (int)(need > 0 ? need : 1);
-  fn<<<grid, 256, 0, st>>>(X, n, w32, out);
+  fn<<<grid, 256, 0, st>>>(X, n, w, out, hist);
   OTF_LAUNCH_CHECK("dense_score_fast");
   return OTF_OK;
 }
 
-int launch_cast_w(const double* w, float* w32, int32_t d, cudaStream_t st) {
-  cast_w_f32<<<(d + 255) / 256, 256, 0, st>>>(w, w32, d);
-  OTF_LAUNCH_CHECK("cast_w_f32");
-  return OTF_OK;
-}
-
-// Scores n rows; w32 is the float32-cast model (device). Pointers must be 16-byte aligned
-// for the fast path (all device buffers this library allocates are).
-int launch_dense_score(const float* X, int64_t n, int32_t d, const float* w32, float* out,
-                       int device, cudaStream_t st) {
+// Scores n rows against the float64 model w (cast to float32 in-kernel). Pointers must be
+// 16-byte aligned for the fast path (all device buffers this library allocates are).
+// hist (nullable): kHistBins counters (zero on entry) receiving the coarse score histogram.
+int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
+                       uint32_t* hist, int device, cudaStream_t st) {
   if (n <= 0) return OTF_OK;
-  const bool aligned = (((uintptr_t)X) & 15) == 0 && (((uintptr_t)w32) & 15) == 0;
+  const bool aligned = (((uintptr_t)X) & 15) == 0;
   if (aligned && d % 128 == 0) {
     switch (d / 128) {
-      case 1: return launch_fast<1, 8>(X, n, w32, out, device, st);
-      case 2: return launch_fast<2, 4>(X, n, w32, out, device, st);
-      case 4: return launch_fast<4, 2>(X, n, w32, out, device, st);
-      case 8: return launch_fast<8, 1>(X, n, w32, out, device, st);
-      case 16: return launch_fast<16, 1>(X, n, w32, out, device, st);
-      case 32: return launch_fast<32, 1>(X, n, w32, out, device, st);
+      case 1: return launch_fast<1, 8>(X, n, w, out, hist, device, st);
+      case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st);
+      case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st);
+      case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st);
+      case 16: return launch_fast<16, 1>(X, n, w, out, hist, device, st);
+      case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st);
       default: break;
     }
   }
   int grid = grid_for((const void*)dense_score_generic, 256, device);
   const int64_t need = (n + 7) / 8;
   if (need < grid) grid = (int)need;
-  dense_score_generic<<<grid, 256, 0, st>>>(X, n, d, w32, out);
+  dense_score_generic<<<grid, 256, 0, st>>>(X, n, d, w, out, hist);
   OTF_LAUNCH_CHECK("dense_score_generic");
   return OTF_OK;
 }

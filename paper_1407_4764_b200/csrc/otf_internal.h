@@ -5,24 +5,28 @@
 
 namespace otf {
 
+// Scoring launchers take the float64 model on the device and (optionally) a kHistBins-entry
+// histogram (zero on entry) that receives the coarse score histogram for launch_topk.
+
 // dense (otf_dense.cu)
-int launch_cast_w(const double* w, float* w32, int32_t d, cudaStream_t st);
-int launch_dense_score(const float* X, int64_t n, int32_t d, const float* w32, float* out,
-                       int device, cudaStream_t st);
+int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
+                       uint32_t* hist, int device, cudaStream_t st);
 
 // pq (otf_pq.cu)
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
                   cudaStream_t st);
 int launch_pq_check(const uint8_t* codes, int64_t total, int K, unsigned int* bad, int device,
                     cudaStream_t st);
-int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const double* lut, int K,
-                   double* out, int device, cudaStream_t st);
+bool pq_fast_path(int M, const uint8_t* codes);
+// fast path builds the LUT in-kernel from (cents, w); the generic path reads `lut`.
+int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, const double* w,
+                   const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
+                   cudaStream_t st);
 
 // binary (otf_binary.cu)
 size_t bin_lut_bytes(int n_bits);
-int launch_bin_lut(const double* w, int n_bits, double* lut, cudaStream_t st);
-int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* lut,
-                     const float* w32, float* out, int device, cudaStream_t st);
+int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
+                     uint32_t* hist, int device, cudaStream_t st);
 int launch_bin_unpack(const uint8_t* codes, int64_t n, int n_bits, float* out, int device,
                       cudaStream_t st);
 int launch_binarize(const double* U, const float* mu, int m, int n_bits, const double* X,
@@ -32,19 +36,21 @@ int launch_hamming(const uint8_t* a, const uint8_t* b, int64_t n, int width, int
 
 // top-k (otf_topk.cu)
 struct TopkWs {
-  uint32_t* hist = nullptr;       // 3 x 256 rotating histograms (zero between calls)
+  uint32_t* hist = nullptr;       // kHistBins coarse histogram (zero between calls)
+  uint32_t* rhist = nullptr;      // 3 x 256 rotating radix histograms (zero between calls)
   unsigned int* bar = nullptr;    // grid barrier {count, generation}
   unsigned int* count = nullptr;  // candidate counter (zero between calls)
   uint64_t* key = nullptr;        // candidate order keys      (cap entries)
   uint64_t* inv = nullptr;        // candidate ~id             (cap entries)
   int64_t* row = nullptr;         // candidate row             (cap entries)
-  int64_t cap = 0;                // power of two >= k_eff
+  int64_t cap = 0;                // power of two >= max(k_eff, kCandCap)
 };
 int topk_ws_alloc(TopkWs* ws, int64_t k_eff);
 void topk_ws_free(TopkWs* ws);
-// scores: float32 (dtype 0) or float64 (dtype 1), n entries on device.
+// scores: float32 (dtype 0) or float64 (dtype 1), n entries on device. If hist_ready, ws->hist
+// already holds the coarse histogram of these scores (fused into the scoring kernel).
 int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, int64_t id_base,
-                int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores,
+                int64_t k_eff, TopkWs* ws, bool hist_ready, int64_t* out_ids, double* out_scores,
                 int64_t* out_rows, int device, cudaStream_t st);
 
 // Pegasos (otf_train.cu)

@@ -95,79 +95,115 @@ __device__ double pairwise_sum(const Get& a, int s, int n) {
   return ret;
 }
 
-struct SmemLut {
+struct GlobalLut {
   const double* lut; int K; const uint8_t* code;
   __device__ __forceinline__ double operator()(int m) const { return lut[m * K + code[m]]; }
 };
 
 // Fast path, compile-time M (M in {4, 8, 16, 32}): one thread per row, codes loaded as
-// 16-byte vectors, LUT (M x 256 float64, zero padded beyond K) in shared memory.
+// vectors, the LUT (M x 256 float64, zero padded beyond K) built per CTA in shared memory
+// straight from the centroids and the float64 w (no separate LUT launch), and the coarse
+// score histogram for the top-k kernel accumulated on the fly.
 template <int M>
 __global__ void __launch_bounds__(256) pq_scan_fast(const uint8_t* __restrict__ codes, int64_t n,
-                                                    const double* __restrict__ lut_g, int K,
-                                                    double* __restrict__ out) {
+                                                    const float* __restrict__ cents,
+                                                    const double* __restrict__ w,
+                                                    const double* __restrict__ lut_g, int K, int Q,
+                                                    double* __restrict__ out,
+                                                    uint32_t* __restrict__ ghist) {
   extern __shared__ double lut[];  // M * 256
+  __shared__ uint32_t sh[kHistBins];
   for (int t = threadIdx.x; t < M * 256; t += blockDim.x) {
     const int m = t >> 8, j = t & 255;
-    lut[t] = j < K ? lut_g[m * K + j] : 0.0;
+    double v = 0.0;
+    if (j < K) v = lut_g ? lut_g[m * K + j]
+                         : lut_entry_einsum(cents + ((int64_t)m * K + j) * Q, w + (int64_t)m * Q, Q);
+    lut[t] = v;
   }
+  if (ghist) hist_zero(sh);
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
-    uint8_t c[M];
-    if constexpr (M >= 16) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t row = base + lane;
+    const bool active = row < n;
+    double res = 0.0;
+    if (active) {
+      uint8_t c[M];
+      if constexpr (M >= 16) {
 #pragma unroll
-      for (int v = 0; v < M / 16; ++v) {
-        uint4 u = ld_stream_u4(reinterpret_cast<const uint4*>(codes + row * M) + v);
-        const uint32_t words[4] = {u.x, u.y, u.z, u.w};
+        for (int v = 0; v < M / 16; ++v) {
+          uint4 u = ld_stream_u4(reinterpret_cast<const uint4*>(codes + row * M) + v);
+          const uint32_t words[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int q = 0; q < 16; ++q) c[16 * v + q] = (words[q >> 2] >> (8 * (q & 3))) & 0xff;
+          for (int q = 0; q < 16; ++q) c[16 * v + q] = (words[q >> 2] >> (8 * (q & 3))) & 0xff;
+        }
+      } else if constexpr (M == 8) {
+        uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + row * M));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[q] = ((q < 4 ? u.x : u.y) >> (8 * (q & 3))) & 0xff;
+      } else {
+        uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(codes + row * M));
+#pragma unroll
+        for (int q = 0; q < M; ++q) c[q] = (u >> (8 * q)) & 0xff;
       }
-    } else if constexpr (M == 8) {
-      uint2 u = __ldg(reinterpret_cast<const uint2*>(codes + row * M));
+      double a[M];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) c[q] = ((q < 4 ? u.x : u.y) >> (8 * (q & 3))) & 0xff;
-    } else {
-      uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(codes + row * M));
+      for (int m = 0; m < M; ++m) a[m] = lut[m * 256 + c[m]];
+      if constexpr (M < 8) {
+        res = -0.0;
 #pragma unroll
-      for (int q = 0; q < M; ++q) c[q] = (u >> (8 * q)) & 0xff;
-    }
-    double a[M];
+        for (int m = 0; m < M; ++m) res = __dadd_rn(res, a[m]);
+      } else {
+        double r[8];
 #pragma unroll
-    for (int m = 0; m < M; ++m) a[m] = lut[m * 256 + c[m]];
-    double res;
-    if constexpr (M < 8) {
-      res = -0.0;
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
 #pragma unroll
-      for (int m = 0; m < M; ++m) res = __dadd_rn(res, a[m]);
-    } else {
-      double r[8];
+        for (int i = 8; i < M; i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = a[j];
-#pragma unroll
-      for (int i = 8; i < M; i += 8) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+          for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
       }
-      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      out[row] = res;
     }
-    out[row] = res;
+    if (ghist) hist_add(sh, active, hist_bin(res));
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
   }
 }
 
-// Generic path: any M, K; LUT read through L1 from global memory.
+// Generic path: any M, K; LUT (built by pq_build_lut_kernel) read through L1.
 __global__ void __launch_bounds__(256) pq_scan_generic(const uint8_t* __restrict__ codes, int64_t n,
                                                        int M, const double* __restrict__ lut,
-                                                       int K, double* __restrict__ out) {
+                                                       int K, double* __restrict__ out,
+                                                       uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kHistBins];
+  if (ghist) hist_zero(sh);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
-    SmemLut g{lut, K, codes + row * M};
-    out[row] = pairwise_sum(g, 0, M);
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t row = base + lane;
+    const bool active = row < n;
+    double res = 0.0;
+    if (active) {
+      GlobalLut g{lut, K, codes + row * M};
+      res = pairwise_sum(g, 0, M);
+      out[row] = res;
+    }
+    if (ghist) hist_add(sh, active, hist_bin(res));
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
   }
 }
 
-// max code per launch -> flag if any code >= K (validation, pq.py:240-241 semantics).
+// flag if any code >= K (validation, pq.py:240-241 semantics).
 __global__ void pq_check_codes(const uint8_t* __restrict__ codes, int64_t total, int K,
                                unsigned int* __restrict__ bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -197,8 +233,9 @@ int launch_pq_check(const uint8_t* codes, int64_t total, int K, unsigned int* ba
 }
 
 template <int M>
-static int launch_fast(const uint8_t* codes, int64_t n, const double* lut, int K, double* out,
-                       int device, cudaStream_t st) {
+static int launch_fast(const uint8_t* codes, int64_t n, const float* cents, const double* w,
+                       const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
+                       cudaStream_t st) {
   auto fn = pq_scan_fast<M>;
   const size_t smem = (size_t)M * 256 * sizeof(double);
   static bool configured[64] = {false};
@@ -212,28 +249,35 @@ static int launch_fast(const uint8_t* codes, int64_t n, const double* lut, int K
   int64_t grid = (int64_t)per_sm * sm_count(device);
   const int64_t need = (n + 255) / 256;
   if (need < grid) grid = need;
-  fn<<<(int)grid, 256, smem, st>>>(codes, n, lut, K, out);
+  fn<<<(int)grid, 256, smem, st>>>(codes, n, cents, w, lut, K, Q, out, hist);
   OTF_LAUNCH_CHECK("pq_scan_fast");
   return OTF_OK;
 }
 
-int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const double* lut, int K,
-                   double* out, int device, cudaStream_t st) {
+bool pq_fast_path(int M, const uint8_t* codes) {
+  return (((uintptr_t)codes) & 15) == 0 && (M == 4 || M == 8 || M == 16 || M == 32);
+}
+
+// Scores n code rows. Fast path: the LUT is built in-kernel from (cents, w) when cents is
+// non-null, else copied from `lut`. Generic path: `lut` must hold the (M, K) table from
+// launch_pq_lut. hist: see launch_dense_score.
+int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, const double* w,
+                   const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
+                   cudaStream_t st) {
   if (n <= 0) return OTF_OK;
-  const bool aligned16 = (((uintptr_t)codes) & 15) == 0;
-  if (aligned16) {
+  if (pq_fast_path(M, codes)) {
     switch (M) {
-      case 4: return launch_fast<4>(codes, n, lut, K, out, device, st);
-      case 8: return launch_fast<8>(codes, n, lut, K, out, device, st);
-      case 16: return launch_fast<16>(codes, n, lut, K, out, device, st);
-      case 32: return launch_fast<32>(codes, n, lut, K, out, device, st);
+      case 4: return launch_fast<4>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
+      case 8: return launch_fast<8>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
+      case 16: return launch_fast<16>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
+      case 32: return launch_fast<32>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
       default: break;
     }
   }
   int64_t grid = (n + 255) / 256;
   const int64_t cap = 8LL * sm_count(device);
   if (grid > cap) grid = cap;
-  pq_scan_generic<<<(int)grid, 256, 0, st>>>(codes, n, M, lut, K, out);
+  pq_scan_generic<<<(int)grid, 256, 0, st>>>(codes, n, M, lut, K, out, hist);
   OTF_LAUNCH_CHECK("pq_scan_generic");
   return OTF_OK;
 }
