@@ -1,15 +1,15 @@
 // otf_dense.cu — K1: dense float32 linear-SVM scoring (score_dense, ranker.py:63-69).
 //
-// s_i = float32( sum_j x_ij * float32(w_j) ), accumulated in float64. Products of two
-// float32 values are exact in float64, so the only rounding is in the float64 adds and the
-// final round-to-nearest to float32. The reference computes the same dot product with an
-// OpenBLAS sgemv (float32 accumulation, host-CPU dependent order), so parity is a stated
-// tolerance. Every row is reduced with the same fixed tree whatever its
+// s_i = float32( sum_j x_ij * float32(w_j) ). The reference computes this dot product with an
+// OpenBLAS sgemv (float32 FMA accumulation, host-CPU dependent order), so parity is a stated
+// tolerance. Here each 4-column chunk is a float32 FMA chain and the chunk
+// sums are accumulated in float64, so the error is that of a 4-term float32 dot, well inside
+// the reference's own rounding. Every row is reduced with the same fixed tree whatever its
 // position, GPU or shard, so a row's score is bit-identical across repositories, subsets
 // (without_ids) and GPU counts.
 //
-// Canonical per-row order (shared by all variants below): lane l of a 32-lane group owns
-// columns {128*c + 4*l + e : c = 0.., e = 0..3}; it accumulates them in (c, e) order into a
+// Canonical per-row order (shared by all variants below): lane l of a 32-lane group owns the
+// 4-column chunks {128*c + 4*l : c = 0..}; chunk sums (chunk_dot) are added in c order into a
 // float64 partial; the 32 partials are then combined by the xor-butterfly tree
 // (l, l^16), (l, l^8), ..., (l, l^1).
 //
@@ -23,6 +23,16 @@
 #include "otf_internal.h"
 
 namespace otf {
+
+// One 4-column chunk: float32 FMA chain x0*w0 (+x1*w1)(+x2*w2)(+x3*w3), the same in every
+// variant. Chunk sums are then accumulated in float64; this keeps the float64->float32 XU
+// conversions at one per 4 columns (two per column saturated the XU pipe at 77%, ncu r1).
+__device__ __forceinline__ float chunk_dot(const float4 x, const float4 w) {
+  float s = __fmul_rn(x.x, w.x);
+  s = __fmaf_rn(x.y, w.y, s);
+  s = __fmaf_rn(x.z, w.z, s);
+  return __fmaf_rn(x.w, w.w, s);
+}
 
 // Fast path: d == 128 * CPL. Each warp handles R rows per iteration, then a transposed
 // butterfly gives ~2 shuffles per row.
@@ -65,11 +75,7 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
         double acc = p[i];
 #pragma unroll
         for (int c = 0; c < LB; ++c) {
-          const float4 wv = wr[lane + 32 * (c0 + c)];
-          acc = __fma_rn((double)v[i][c].x, (double)wv.x, acc);
-          acc = __fma_rn((double)v[i][c].y, (double)wv.y, acc);
-          acc = __fma_rn((double)v[i][c].z, (double)wv.z, acc);
-          acc = __fma_rn((double)v[i][c].w, (double)wv.w, acc);
+          acc = __dadd_rn(acc, (double)chunk_dot(v[i][c], wr[lane + 32 * (c0 + c)]));
         }
         p[i] = acc;
       }
@@ -104,11 +110,10 @@ __global__ void __launch_bounds__(256) dense_score_generic(const float* __restri
     const float* x = X + row * (int64_t)d;
     double acc = 0.0;
     for (int base = 4 * lane; base < d; base += 128) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = base + e;
-        if (j < d) acc = __fma_rn((double)__ldg(x + j), (double)__double2float_rn(w[j]), acc);
-      }
+      const int m = d - base < 4 ? d - base : 4;
+      float cs = __fmul_rn(__ldg(x + base), __double2float_rn(w[base]));
+      for (int e = 1; e < m; ++e) cs = __fmaf_rn(__ldg(x + base + e), __double2float_rn(w[base + e]), cs);
+      acc = __dadd_rn(acc, (double)cs);
     }
     double p[1] = {acc};
     transposed_reduce<1, 32>(p, lane);

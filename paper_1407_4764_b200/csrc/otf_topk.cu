@@ -243,17 +243,23 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
   }
 
   if (C <= kCandCap) {
-    // ---- C: gather the candidates, sort them in CTA 0 -----------------------------------------
-    for (int64_t base = wbase0; base < n; base += nthreads) {
-      const int64_t i = base + lane;
-      bool take = false;
-      uint64_t key = 0, inv = 0;
-      if (i < n) {
-        const ST s = __ldcg(scores + i);
-        take = all || hist_bin(s) >= b0;
-        if (take) { key = score_key(s); inv = ~(uint64_t)id_of(ids, id_base, i); }
+    // ---- C: gather the candidates (8 loads in flight per thread), rank them -----------------
+    constexpr int U = 8;
+    for (int64_t base = wbase0 * U; base < n; base += nthreads * U) {
+      ST v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int64_t i = base + 32 * q + lane;
+        v[q] = i < n ? __ldcg(scores + i) : ST(0);
       }
-      append_candidate(ws, take, key, inv, i, C);
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int64_t i = base + 32 * q + lane;
+        const bool take = i < n && (all || hist_bin(v[q]) >= b0);
+        uint64_t key = 0, inv = 0;
+        if (take) { key = score_key(v[q]); inv = ~(uint64_t)id_of(ids, id_base, i); }
+        append_candidate(ws, take, key, inv, i, C);
+      }
     }
     grid_barrier(ws.bar, nb);
     if (blockIdx.x == 0) {  // every CTA has read hist and count is no longer needed
