@@ -114,7 +114,7 @@ struct otf_repo {
   float* cents = nullptr;          // pq centroids (device)
   cudaStream_t stream = nullptr;
   std::mutex mu;                   // one call at a time per handle
-  DevBuf w, w32, lut, scores, outbuf;
+  DevBuf w, w32, lut, scores, bins, outbuf;
   HostBuf h_w, h_out;
   TopkWs topk;
   // graph cache for otf_repo_rank_graph
@@ -202,7 +202,7 @@ void repo_free(otf_repo* r) {
   if (r->owns_payload && r->payload) cudaFree(const_cast<void*>(r->payload));
   if (r->ids) cudaFree(r->ids);
   if (r->cents) cudaFree(r->cents);
-  r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->outbuf.release();
+  r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->bins.release(); r->outbuf.release();
   r->h_w.release(); r->h_out.release();
   topk_ws_free(&r->topk);
   if (r->stream) cudaStreamDestroy(r->stream);
@@ -233,14 +233,14 @@ int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStr
     return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dw,
                               static_cast<float*>(out), hist, r->device, st);
   if (r->kind == OTF_KIND_PQ) {
+    // the (M, K) float64 LUT is built once per query (one thread per entry), then every scan
+    // CTA copies it into shared memory instead of re-deriving it
     const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
-    if (!pq_fast_path(r->M, codes)) {  // generic path reads a separately built LUT
-      if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
-      if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
-        return rc;
-    }
-    return launch_pq_scan(codes, r->n, r->M, r->cents, dw, static_cast<const double*>(r->lut.p), r->K,
-                          r->Q, static_cast<double*>(out), hist, r->device, st);
+    if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
+    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
+      return rc;
+    return launch_pq_scan(codes, r->n, r->M, nullptr, nullptr, static_cast<const double*>(r->lut.p),
+                          r->K, r->Q, static_cast<double*>(out), hist, r->device, st);
   }
   return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, dw,
                           static_cast<float*>(out), hist, r->device, st);
@@ -255,6 +255,21 @@ int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, doub
   int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
   if (rc) return rc;
   if ((rc = topk_ws_alloc(&r->topk, k_eff))) return rc;
+  const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
+  if (r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes)) {
+    // PQ: the scan writes 2-byte bins, the top-k recomputes the candidates' exact scores
+    if ((rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t)))) return rc;
+    if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
+    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
+      return rc;
+    if ((rc = launch_pq_scan_bins(codes, r->n, static_cast<const double*>(r->lut.p), r->K,
+                                  static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st)))
+      return rc;
+    return launch_topk_pq_bins(static_cast<const uint16_t*>(r->bins.p), codes, r->M,
+                               static_cast<const double*>(r->lut.p), r->K, r->n, r->ids, r->id_base,
+                               k_eff, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows,
+                               r->device, st);
+  }
   const bool fuse = k_eff < r->n;
   if ((rc = score_into(r, dw, r->scores.p, fuse ? r->topk.hist : nullptr, st))) return rc;
   return launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, fuse,
@@ -478,6 +493,7 @@ int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* id
     if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
     if (!rc) rc = r->w32.ensure((size_t)r->model_dim * sizeof(float));
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
+    if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
     if (!rc && (r->kind == OTF_KIND_BINARY) && bin_lut_bytes(r->model_dim))
       rc = r->lut.ensure(bin_lut_bytes(r->model_dim));
     if (rc) return rc;

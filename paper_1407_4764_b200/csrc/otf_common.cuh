@@ -61,13 +61,11 @@ __device__ __forceinline__ uint32_t hist_bin(double s) { return hist_bin(__doubl
 __device__ __forceinline__ void hist_zero(uint32_t* sh) {
   for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0u;
 }
-// Warp-aggregated shared-memory histogram update; must be called by all 32 lanes.
+// Shared-memory histogram update. Plain per-lane ATOMS: the scores of neighbouring rows
+// rarely share a bin, and __match_any_sync (ADU pipe) cost more than the replays it saves
+// (57% ADU utilisation in the r1 PQ profile).
 __device__ __forceinline__ void hist_add(uint32_t* sh, bool active, uint32_t bin) {
-  const unsigned act = __ballot_sync(0xffffffffu, active);
-  if (act == 0u) return;
-  const unsigned peers = __match_any_sync(0xffffffffu, active ? bin : 0xffffffffu);
-  const int lane = threadIdx.x & 31;
-  if (active && lane == __ffs(peers) - 1) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+  if (active) atomicAdd(&sh[bin], 1u);
 }
 __device__ __forceinline__ void hist_flush(const uint32_t* sh, uint32_t* g) {
   for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)

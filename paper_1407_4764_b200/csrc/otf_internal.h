@@ -18,6 +18,10 @@ int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, doub
 int launch_pq_check(const uint8_t* codes, int64_t total, int K, unsigned int* bad, int device,
                     cudaStream_t st);
 bool pq_fast_path(int M, const uint8_t* codes);
+// M == 16 fast path can emit 16-bit score bins instead of float64 scores (rank path).
+bool pq_bins_path(int M, const uint8_t* codes);
+int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
+                        uint32_t* hist, int device, cudaStream_t st);
 // fast path builds the LUT in-kernel from (cents, w); the generic path reads `lut`.
 int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, const double* w,
                    const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
@@ -52,6 +56,12 @@ void topk_ws_free(TopkWs* ws);
 int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, int64_t id_base,
                 int64_t k_eff, TopkWs* ws, bool hist_ready, int64_t* out_ids, double* out_scores,
                 int64_t* out_rows, int device, cudaStream_t st);
+// PQ rank path: per-row bins (+ fused histogram) from launch_pq_scan_bins; exact float64 scores
+// of candidates recomputed from codes + lut. scratch: n float64 (used only on the rare path).
+int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,
+                        int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, TopkWs* ws,
+                        double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+                        int device, cudaStream_t st);
 
 // Pegasos (otf_train.cu)
 int launch_pegasos(double* w, int d, const void* pos, int pos_dtype, int64_t n_pos,

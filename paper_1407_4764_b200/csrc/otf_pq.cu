@@ -270,8 +270,12 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
                                                      const double* __restrict__ w,
                                                      const double* __restrict__ lut_g, int K, int Q,
                                                      double* __restrict__ out,
+                                                     uint16_t* __restrict__ bins_out,
                                                      uint32_t* __restrict__ ghist) {
-  extern __shared__ double lut[];  // 256 * 16, entry (m, j) at j*16 + m
+  // bins_out != nullptr: write the 16-bit score bin per row instead of the float64 score (the
+  // top-k kernel recomputes the exact score of the few candidates; otf_topk.cu PqBinSrc).
+  // static (not dynamic) shared memory so the LUT base is an immediate in every LDS
+  __shared__ __align__(128) double lut[256 * 16];  // entry (m, j) at byte (j << 7) | (m << 3)
   __shared__ uint32_t sh[kHistBins];
   for (int t = threadIdx.x; t < 16 * 256; t += blockDim.x) {
     const int m = t >> 8, j = t & 255;
@@ -284,6 +288,10 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t s = lane & 15;
+  uint32_t cm[16];  // byte offset of sub-quantizer table t ^ s inside a 128-byte LUT line
+#pragma unroll
+  for (int t = 0; t < 16; ++t) cm[t] = ((uint32_t)t ^ s) << 3;
+  const char* lutb = reinterpret_cast<const char*>(lut);
   const uint4* C4 = reinterpret_cast<const uint4*>(codes);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * ROWS; base < n;
@@ -312,16 +320,21 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
       double b[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
-        const uint32_t j = (wd[t >> 2] >> (8 * (t & 3))) & 0xffu;
-        b[t] = lut[j * 16 + ((uint32_t)t ^ s)];
+        const int q = t & 3;  // byte q of the word, moved to bits [7, 15) = code << 7
+        const uint32_t hi = q == 0 ? (wd[t >> 2] << 7) : (wd[t >> 2] >> (8 * q - 7));
+        b[t] = *reinterpret_cast<const double*>(lutb + ((hi & 0x7F80u) | cm[t]));
       }
       double r[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) r[t] = __dadd_rn(b[t], b[t + 8]);
       const double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                                    __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-      if (active) out[row] = res;
-      if (ghist) hist_add(sh, active, hist_bin(res));
+      const uint32_t bin = hist_bin(res);
+      if (active) {
+        if (bins_out) bins_out[row] = (uint16_t)bin;
+        else out[row] = res;
+      }
+      if (ghist) hist_add(sh, active, bin);
     }
   }
   if (ghist) {
@@ -331,29 +344,31 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
 }
 
 static int launch_scan16(const uint8_t* codes, int64_t n, const float* cents, const double* w,
-                         const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
-                         cudaStream_t st) {
+                         const double* lut, int K, int Q, double* out, uint16_t* bins,
+                         uint32_t* hist, int device, cudaStream_t st) {
   constexpr int ROWS = 4;
-  auto fn = pq_scan16_xor<ROWS>;
-  const size_t smem = (size_t)16 * 256 * sizeof(double);
-  static bool configured[64] = {false};
-  if (!configured[device & 63]) {
-    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured[device & 63] = true;
-  }
+  auto fn = pq_scan16_xor<ROWS>;  // 48 KB static shared memory (LUT + histogram)
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sm_count(device);
   const int64_t need = (n + 256 * ROWS - 1) / (256 * ROWS);
   if (need < grid) grid = need;
-  fn<<<(int)grid, 256, smem, st>>>(codes, n, cents, w, lut, K, Q, out, hist);
+  fn<<<(int)grid, 256, 0, st>>>(codes, n, cents, w, lut, K, Q, out, bins, hist);
   OTF_LAUNCH_CHECK("pq_scan16_xor");
   return OTF_OK;
 }
 
 bool pq_fast_path(int M, const uint8_t* codes) {
   return (((uintptr_t)codes) & 15) == 0 && (M == 4 || M == 8 || M == 16 || M == 32);
+}
+
+bool pq_bins_path(int M, const uint8_t* codes) { return M == 16 && pq_fast_path(M, codes); }
+
+int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
+                        uint32_t* hist, int device, cudaStream_t st) {
+  if (n <= 0) return OTF_OK;
+  return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
 }
 
 // Scores n code rows. Fast path: the LUT is built in-kernel from (cents, w) when cents is
@@ -367,7 +382,7 @@ int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, c
     switch (M) {
       case 4: return launch_fast<4>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
       case 8: return launch_fast<8>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
-      case 16: return launch_scan16(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
+      case 16: return launch_scan16(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, nullptr, hist, device, st);
       case 32: return launch_fast<32>(codes, n, cents, w, cents ? nullptr : lut, K, Q, out, hist, device, st);
       default: break;
     }

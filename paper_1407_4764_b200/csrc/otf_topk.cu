@@ -17,14 +17,19 @@
 //      on the full order key, 8 bits per pass with a grid barrier each, then on ~id inside a
 //      tied key; gather exactly k_eff entries and rank them (or a global bitonic sort when
 //      k_eff > 8192).
-// Scores are read from L2 (the scoring kernel just wrote them); the common case reads them
-// once (phase C) after the fused histogram.
+//
+// Score sources: DirectSrc reads a score array the scoring kernel wrote (dense / binary float32,
+// generic float64). PqBinSrc is the PQ fast path: the scan kernel writes only a 16-bit bin per
+// row (2 B instead of 8 B) plus the histogram, and the exact float64 score of a candidate is
+// recomputed here from its codes and the LUT (numpy order, bit-identical to the scan) — so the
+// gather reads 2 B/row. Phase D first materialises all exact scores for such a source.
 #include "otf_common.cuh"
 #include "otf_internal.h"
 
 namespace otf {
 
 static constexpr int kTopkThreads = 1024;
+static constexpr int kTopkCtasPerSm = 1;
 static constexpr int kCandCap = 8192;                       // candidates ranked in smem
 static constexpr size_t kTopkSmem = (size_t)kCandCap * 16;  // key + inv per candidate
 
@@ -50,11 +55,6 @@ __device__ __forceinline__ int64_t id_of(const int64_t* ids, int64_t id_base, in
   return ids ? ids[row] : id_base + row;
 }
 
-template <typename ST>
-__device__ __forceinline__ uint64_t load_key(const ST* s, int64_t i) {
-  return score_key(__ldcg(s + i));
-}
-
 __device__ __forceinline__ bool cand_greater(uint64_t ka, uint64_t ia, uint64_t kb, uint64_t ib) {
   return ka > kb || (ka == kb && ia > ib);
 }
@@ -64,6 +64,69 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+
+// Inverse of score_key(double) (exact: the key is a bijection except -0.0 -> +0.0).
+__device__ __forceinline__ double key_to_f64(uint64_t k) {
+  const uint64_t u = (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// ---- score sources ---------------------------------------------------------------------------
+template <typename ST>
+struct DirectSrc {
+  using T = ST;
+  static constexpr int kLoadBytes = sizeof(ST);
+  const ST* s;
+  __device__ __forceinline__ ST load(int64_t i) const { return __ldcg(s + i); }
+  // 8 consecutive entries from i (i % 8 == 0): two float4 / four double2 loads.
+  __device__ __forceinline__ void load8(int64_t i, ST (&v)[8]) const {
+    if constexpr (sizeof(ST) == 4) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(s + i));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(s + i) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 a = __ldcg(reinterpret_cast<const double2*>(s + i) + q);
+        v[2 * q] = a.x; v[2 * q + 1] = a.y;
+      }
+    }
+  }
+  __device__ __forceinline__ uint32_t bin_of(ST v) const { return hist_bin(v); }
+  __device__ __forceinline__ ST exact(int64_t, ST v) const { return v; }
+  __device__ __forceinline__ double out_score(int64_t row, uint64_t) const {
+    return (double)__ldcg(s + row);  // keeps a caller's -0.0 bit pattern
+  }
+};
+
+struct PqBinSrc {
+  using T = double;
+  static constexpr int kLoadBytes = 2;
+  const uint16_t* bins; const uint8_t* codes; const double* lut; int M, K;
+  __device__ __forceinline__ uint32_t load(int64_t i) const { return __ldcg(bins + i); }
+  __device__ __forceinline__ void load8(int64_t i, uint32_t (&v)[8]) const {
+    const uint4 a = __ldcg(reinterpret_cast<const uint4*>(bins + i));
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { v[2 * q] = w[q] & 0xffffu; v[2 * q + 1] = w[q] >> 16; }
+  }
+  __device__ __forceinline__ uint32_t bin_of(uint32_t v) const { return v; }
+  // M == 16 (the only bins-path shape): one 16-byte code load, 16 independent LUT loads, then
+  // numpy's pairwise tree (r_j = a_j + a_{j+8}, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))).
+  __device__ __forceinline__ double exact(int64_t i, uint32_t) const {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(codes + i * 16));
+    const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+    double a[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) a[m] = __ldg(lut + m * K + ((wd[m >> 2] >> (8 * (m & 3))) & 0xffu));
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(a[j], a[j + 8]);
+    return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                     __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  }
+  __device__ __forceinline__ double out_score(int64_t, uint64_t key) const { return key_to_f64(key); }
+};
 
 // Appends (key, ~id, row) for every lane with `take`, one atomic per warp.
 __device__ __forceinline__ void append_candidate(const TopkWs& ws, bool take, uint64_t key,
@@ -84,13 +147,14 @@ __device__ __forceinline__ void append_candidate(const TopkWs& ws, bool take, ui
 }
 
 // Block-wide: bins scanned from 4095 down; finds the bin where the running count reaches
-// `need`. Thread t owns bins 4095-4t .. 4092-4t.
+// `need`. Thread t owns bins 4095-BPT*t .. 4096-BPT*(t+1).
+constexpr int kBPT = kHistBins / kTopkThreads;
 __device__ void find_bin4096(const uint32_t* h, int64_t need, int* out_b, int64_t* out_above,
                              int64_t* out_cnt, int64_t* wsum) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   int64_t local = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) local += h[4095 - 4 * t - q];
+  for (int q = 0; q < kBPT; ++q) local += h[4095 - kBPT * t - q];
   int64_t incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -114,8 +178,8 @@ __device__ void find_bin4096(const uint32_t* h, int64_t need, int* out_b, int64_
   const int64_t excl = incl - local;
   if (excl < need && incl >= need) {
     int64_t cum = excl;
-    for (int q = 0; q < 4; ++q) {
-      const int bin = 4095 - 4 * t - q;
+    for (int q = 0; q < kBPT; ++q) {
+      const int bin = 4095 - kBPT * t - q;
       if (cum + h[bin] >= need) {
         *out_b = bin;
         *out_above = cum;
@@ -164,8 +228,8 @@ __device__ __forceinline__ void pick_bin256(const uint32_t* h, int64_t need, int
 // i == blockIdx.x (mod gridDim.x), one warp per candidate; candidates with rank < k_eff are
 // written straight to their output slot. O(m^2 / #SMs) comparisons, no sorting network, no
 // barrier — the whole grid shares the work (m <= kCandCap).
-template <typename ST>
-__device__ void rank_emit(const ST* scores, const TopkWs& ws, int64_t m, int64_t k_eff,
+template <typename Src>
+__device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k_eff,
                           unsigned char* dyn, int64_t* out_ids, double* out_scores,
                           int64_t* out_rows) {
   const int64_t mine = m > blockIdx.x ? (m - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -188,89 +252,24 @@ __device__ void rank_emit(const ST* scores, const TopkWs& ws, int64_t m, int64_t
     if (lane == 0 && cnt < k_eff) {
       const int64_t r = __ldcg(ws.row + i);
       out_ids[cnt] = (int64_t)~ii;
-      out_scores[cnt] = (double)__ldcg(scores + r);
+      out_scores[cnt] = src.out_score(r, ki);
       if (out_rows) out_rows[cnt] = r;
     }
   }
 }
 
-template <typename ST>
-__global__ void __launch_bounds__(kTopkThreads, 1)
-topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __restrict__ ids,
-                 int64_t id_base, int64_t k_eff, TopkWs ws, int hist_ready,
-                 int64_t* __restrict__ out_ids, double* __restrict__ out_scores,
-                 int64_t* __restrict__ out_rows) {
+// Phase D over a materialised score array (see header). Returns after writing the output.
+template <typename ST, typename Src>
+__device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, const int64_t* ids,
+                                  int64_t id_base, int64_t k_eff, const TopkWs& ws, bool all,
+                                  unsigned char* dyn, int64_t* out_ids, double* out_scores,
+                                  int64_t* out_rows, uint32_t* h, int* s_b, int64_t* s_above) {
   constexpr int KB = KeyBits<ST>::value;
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ uint32_t h[256];
-  __shared__ int s_b;
-  __shared__ int64_t s_above, s_cnt;
-  __shared__ int64_t wsum[32];
   const unsigned int nb = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  const bool all = k_eff >= n;
-
-  // ---- A: coarse histogram (skipped when fused into the scoring kernel) --------------------
-  if (!all && !hist_ready) {
-    uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
-    hist_zero(sh);
-    __syncthreads();
-    for (int64_t base = wbase0; base < n; base += nthreads) {
-      const int64_t i = base + lane;
-      const bool active = i < n;
-      hist_add(sh, active, active ? hist_bin(__ldcg(scores + i)) : 0u);
-    }
-    __syncthreads();
-    hist_flush(sh, ws.hist);
-    grid_barrier(ws.bar, nb);
-  }
-
-  // ---- B: the bin holding the k-th entry ------------------------------------------------------
-  int64_t C = n;
-  uint32_t b0 = 0;
-  if (!all) {
-    uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = __ldcg(ws.hist + b);
-    __syncthreads();
-    find_bin4096(sh, k_eff, &s_b, &s_above, &s_cnt, wsum);
-    __syncthreads();
-    b0 = (uint32_t)s_b;
-    C = s_above + s_cnt;
-    __syncthreads();
-  }
-
-  if (C <= kCandCap) {
-    // ---- C: gather the candidates (8 loads in flight per thread), rank them -----------------
-    constexpr int U = 8;
-    for (int64_t base = wbase0 * U; base < n; base += nthreads * U) {
-      ST v[U];
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int64_t i = base + 32 * q + lane;
-        v[q] = i < n ? __ldcg(scores + i) : ST(0);
-      }
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int64_t i = base + 32 * q + lane;
-        const bool take = i < n && (all || hist_bin(v[q]) >= b0);
-        uint64_t key = 0, inv = 0;
-        if (take) { key = score_key(v[q]); inv = ~(uint64_t)id_of(ids, id_base, i); }
-        append_candidate(ws, take, key, inv, i, C);
-      }
-    }
-    grid_barrier(ws.bar, nb);
-    if (blockIdx.x == 0) {  // every CTA has read hist and count is no longer needed
-      for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
-      if (threadIdx.x == 0) *ws.count = 0u;
-    }
-    rank_emit(scores, ws, C, k_eff, dyn, out_ids, out_scores, out_rows);
-    return;
-  }
-
-  // ---- D: exact MSD radix select on the full key, then on ~id within a tied key ------------
   uint64_t pre = 0, msk = 0, pre2 = 0, msk2 = 0;
   int64_t need = k_eff;
   int phase = all ? 2 : 0;  // k_eff == n: everything is gathered (mask 0)
@@ -284,12 +283,12 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
     __syncthreads();
     if (phase == 0) {
       for (int64_t i = tid; i < n; i += nthreads) {
-        const uint64_t key = load_key(scores, i);
+        const uint64_t key = score_key(__ldcg(scores + i));
         if ((key & msk) == pre) atomicAdd(&h[(key >> shift) & 255u], 1u);
       }
     } else {
       for (int64_t i = tid; i < n; i += nthreads) {
-        const uint64_t key = load_key(scores, i);
+        const uint64_t key = score_key(__ldcg(scores + i));
         if (key == pre) {
           const uint64_t inv = ~(uint64_t)id_of(ids, id_base, i);
           if ((inv & msk2) == pre2) atomicAdd(&h[(inv >> shift) & 255u], 1u);
@@ -301,10 +300,10 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
     grid_barrier(ws.bar, nb);
     if (threadIdx.x < 256) h[threadIdx.x] = __ldcg(H + threadIdx.x);
     __syncthreads();
-    pick_bin256(h, need, &s_b, &s_above);
+    pick_bin256(h, need, s_b, s_above);
     __syncthreads();
-    const int b = s_b;
-    need -= s_above;
+    const int b = *s_b;
+    need -= *s_above;
     const uint32_t cnt = h[b];
     if (phase == 0) {
       pre |= (uint64_t)b << shift;
@@ -329,7 +328,7 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
     bool in = false;
     uint64_t key = 0, inv = 0;
     if (i < n) {
-      key = load_key(scores, i);
+      key = score_key(__ldcg(scores + i));
       const uint64_t mk = key & msk;
       inv = ~(uint64_t)id_of(ids, id_base, i);
       in = mk > pre || (mk == pre && (!tie || (inv & msk2) >= pre2));
@@ -343,7 +342,7 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
   }
   if (k_eff <= kCandCap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *ws.count = 0u;
-    rank_emit(scores, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows);
+    rank_emit(src, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows);
     return;
   }
   // global bitonic sort over ws (capacity P)
@@ -374,10 +373,117 @@ topk_coop_kernel(const ST* __restrict__ scores, int64_t n, const int64_t* __rest
   for (int64_t t = tid; t < k_eff; t += nthreads) {
     const int64_t r = __ldcg(ws.row + t);
     out_ids[t] = (int64_t)~__ldcg(ws.inv + t);
-    out_scores[t] = (double)__ldcg(scores + r);
+    out_scores[t] = src.out_score(r, __ldcg(ws.key + t));
     if (out_rows) out_rows[t] = r;
   }
   if (tid == 0) *ws.count = 0u;
+}
+
+template <typename Src>
+__global__ void __launch_bounds__(kTopkThreads, kTopkCtasPerSm)
+topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id_base,
+                 int64_t k_eff, TopkWs ws, int hist_ready, typename Src::T* scratch,
+                 int64_t* __restrict__ out_ids, double* __restrict__ out_scores,
+                 int64_t* __restrict__ out_rows) {
+  using ST = typename Src::T;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ uint32_t h[256];
+  __shared__ int s_b;
+  __shared__ int64_t s_above, s_cnt;
+  __shared__ int64_t wsum[32];
+  const unsigned int nb = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const bool all = k_eff >= n;
+
+  // ---- A: coarse histogram (skipped when fused into the scoring kernel) --------------------
+  if (!all && !hist_ready) {
+    uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
+    hist_zero(sh);
+    __syncthreads();
+    for (int64_t base = wbase0; base < n; base += nthreads) {
+      const int64_t i = base + lane;
+      if (i < n) hist_add(sh, true, src.bin_of(src.load(i)));
+    }
+    __syncthreads();
+    hist_flush(sh, ws.hist);
+    grid_barrier(ws.bar, nb);
+  }
+
+  // ---- B: the bin holding the k-th entry ------------------------------------------------------
+  int64_t C = n;
+  uint32_t b0 = 0;
+  if (!all) {
+    uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = __ldcg(ws.hist + b);
+    __syncthreads();
+    find_bin4096(sh, k_eff, &s_b, &s_above, &s_cnt, wsum);
+    __syncthreads();
+    b0 = (uint32_t)s_b;
+    C = s_above + s_cnt;
+    __syncthreads();
+  }
+
+  if (C <= kCandCap) {
+    // ---- C: gather the candidates, rank them ----------------------------------------------------
+    // Each lane reads 8 consecutive entries with vector loads (a warp covers 256 contiguous
+    // entries); candidates are rare (C out of n), so one warp vote skips the append path.
+    // Each lane reads R groups of 8 consecutive entries per iteration (R*8 entries in flight).
+    constexpr int U = 8;
+    constexpr int R = 1;  // more groups spill at 64 registers (1024 threads) and ran slower
+    using V = decltype(src.load(0));
+    for (int64_t wb = wbase0 * U * R; wb < n; wb += nthreads * U * R) {  // warp-uniform loop
+      V v[R][U];
+#pragma unroll
+      for (int g = 0; g < R; ++g) {
+        const int64_t base = wb + (int64_t)(g * 32 + lane) * U;
+        if (base + U <= n) {
+          src.load8(base, v[g]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < U; ++q) v[g][q] = base + q < n ? src.load(base + q) : V(0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < R; ++g) {
+        const int64_t base = wb + (int64_t)(g * 32 + lane) * U;
+        unsigned takes = 0;
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if (base + q < n && (all || src.bin_of(v[g][q]) >= b0)) takes |= 1u << q;
+        if (__any_sync(0xffffffffu, takes != 0u)) {
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const bool take = (takes >> q) & 1u;
+            uint64_t key = 0, inv = 0;
+            if (take) {
+              key = score_key(src.exact(base + q, v[g][q]));
+              inv = ~(uint64_t)id_of(ids, id_base, base + q);
+            }
+            append_candidate(ws, take, key, inv, base + q, C);
+          }
+        }
+      }
+    }
+    grid_barrier(ws.bar, nb);
+    if (blockIdx.x == 0) {  // every CTA has read hist and count is no longer needed
+      for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
+      if (threadIdx.x == 0) *ws.count = 0u;
+    }
+    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows);
+    return;
+  }
+
+  // ---- D: exact radix select over a materialised score array --------------------------------
+  const ST* scores = scratch;
+  if (Src::kLoadBytes == 2) {  // bins-only source: compute every exact score once
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthreads)
+      scratch[i] = src.exact(i, src.load(i));
+    grid_barrier(ws.bar, nb);
+  }
+  radix_select_emit(scores, src, n, ids, id_base, k_eff, ws, all, dyn, out_ids, out_scores, out_rows,
+                    h, &s_b, &s_above);
 }
 
 int topk_ws_alloc(TopkWs* ws, int64_t k_eff) {
@@ -407,18 +513,18 @@ void topk_ws_free(TopkWs* ws) {
   *ws = TopkWs{};
 }
 
-template <typename ST>
-static int launch_typed(const ST* scores, int64_t n, const int64_t* ids, int64_t id_base,
-                        int64_t k_eff, TopkWs* ws, bool hist_ready, int64_t* out_ids,
-                        double* out_scores, int64_t* out_rows, int device, cudaStream_t st) {
-  auto fn = topk_coop_kernel<ST>;
+template <typename Src>
+static int launch_src(const Src& src, int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff,
+                      TopkWs* ws, bool hist_ready, typename Src::T* scratch, int64_t* out_ids,
+                      double* out_scores, int64_t* out_rows, int device, cudaStream_t st) {
+  auto fn = topk_coop_kernel<Src>;
   static bool configured[64] = {false};
   if (!configured[device & 63]) {
     OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kTopkSmem));
     configured[device & 63] = true;
   }
-  int grid = sm_count(device);
+  int grid = sm_count(device) * kTopkCtasPerSm;
   const int64_t useful = (n + kTopkThreads - 1) / kTopkThreads;
   if (useful < grid) grid = (int)(useful > 0 ? useful : 1);
   cudaLaunchConfig_t cfg = {};
@@ -431,7 +537,7 @@ static int launch_typed(const ST* scores, int64_t n, const int64_t* ids, int64_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, scores, n, ids, id_base, k_eff, *ws, (int)hist_ready,
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, src, n, ids, id_base, k_eff, *ws, (int)hist_ready, scratch,
                               out_ids, out_scores, out_rows));
   count_launch();
   return OTF_OK;
@@ -443,11 +549,26 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
   if (k_eff <= 0 || n <= 0) return OTF_OK;
   int rc = topk_ws_alloc(ws, k_eff);
   if (rc) return rc;
-  if (dtype == OTF_F32)
-    return launch_typed(static_cast<const float*>(scores), n, ids, id_base, k_eff, ws, hist_ready,
-                        out_ids, out_scores, out_rows, device, st);
-  return launch_typed(static_cast<const double*>(scores), n, ids, id_base, k_eff, ws, hist_ready,
-                      out_ids, out_scores, out_rows, device, st);
+  if (dtype == OTF_F32) {
+    DirectSrc<float> src{static_cast<const float*>(scores)};
+    return launch_src(src, n, ids, id_base, k_eff, ws, hist_ready, const_cast<float*>(src.s), out_ids,
+                      out_scores, out_rows, device, st);
+  }
+  DirectSrc<double> src{static_cast<const double*>(scores)};
+  return launch_src(src, n, ids, id_base, k_eff, ws, hist_ready, const_cast<double*>(src.s), out_ids,
+                    out_scores, out_rows, device, st);
+}
+
+int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,
+                        int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, TopkWs* ws,
+                        double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+                        int device, cudaStream_t st) {
+  if (k_eff <= 0 || n <= 0) return OTF_OK;
+  int rc = topk_ws_alloc(ws, k_eff);
+  if (rc) return rc;
+  PqBinSrc src{bins, codes, lut, M, K};
+  return launch_src(src, n, ids, id_base, k_eff, ws, true, scratch, out_ids, out_scores, out_rows,
+                    device, st);
 }
 
 }  // namespace otf
