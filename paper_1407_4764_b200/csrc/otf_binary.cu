@@ -4,99 +4,95 @@
 // Scoring: s_i = float32( sum_{j < n_bits, bit j set} float32(w_j) ), bit j = byte j/8,
 // bit j%8 (LSB first); padding bits are ignored (the reference unpacks with
 // count=output_bits). Instead of unpacking 2048 bits to floats (the reference's 32x
-// expansion) each 4-bit nibble indexes a 16-entry float64 table T_p[v] = sum of the
-// float32 weights of the set bits of v (added in bit order, exact in float64 for any
-// realistic weight range). The tables live in shared memory laid out so that every lane of
-// a half-warp reads its own bank pair (conflict-free); the per-row sum uses a fixed lane
-// tree (as in otf_dense.cu), so a row's score does not depend on its position.
+// expansion) each code byte indexes a 256-entry table of the summed weights of its set bits
+// (bin_score_bytes below: one conflict-free 4-byte shared-memory lookup per code byte). The
+// per-row sum uses a fixed lane tree (as in otf_dense.cu), so a row's score does not depend
+// on its position. Parity with the reference's float32 sgemv is a tolerance.
 //
-// HBM roofline: n_bits/8 bytes per row (256 B for 2048-bit codes). The nibble lookups
-// (512 per 2048-bit row) make this kernel shared-memory bound at ~35% of HBM.
+// HBM roofline: n_bits/8 bytes per row (256 B for 2048-bit codes).
 #include "otf_common.cuh"
 #include "otf_internal.h"
 
 namespace otf {
 
-// Table layout for the fast path: codes are read as 16-byte chunks; lane l of a 16-lane
-// group owns chunks {l + 16*t}. Nibble i (0..31) of chunk c has value v; its table entry
-// T[c][i][v] is stored at double index ((t*32 + i)*16 + v)*16 + (c % 16), with t = c/16,
-// so the 16 lanes of a half-warp always hit 16 distinct bank pairs.
-__device__ __forceinline__ double nibble_entry(const double* __restrict__ w, int n_bits, int e,
-                                               int* slot) {
-  const int v = e & 15;
-  const int i = (e >> 4) & 31;
-  const int c = e >> 9;
-  const int bit0 = c * 128 + i * 4;
-  double s = 0.0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int j = bit0 + b;
-    if ((v >> b) & 1) s = __dadd_rn(s, j < n_bits ? (double)__double2float_rn(w[j]) : 0.0);
-  }
-  const int t = c >> 4, lane = c & 15;
-  *slot = ((t * 32 + i) * 16 + v) * 16 + lane;
-  return s;
-}
+// Byte-table fast path (rows of RB bytes, RB % 128 == 0, e.g. 2048-bit codes = 256 B).
+// A pass covers one 128-byte slice of every row: lane l reads the 4-byte word at slice offset
+// 4l (one coalesced 128 B load per row per warp) and looks up each byte b_k (k = 0..3) in a
+// float32 table T_{l,k}[v] = float32(sum of the float32 weights of the set bits of v)
+// (summed in float64, bit order). Table entry (k, v, l) sits at byte address
+//   (k >> 1) << 16 | v << 8 | (k & 1) << 7 | l << 2
+// so every lane reads its own bank (conflict-free) and the whole address is ONE byte_perm of
+// the code word with a per-lane constant (no shift/mask arithmetic per lookup). The 4 lane
+// values are summed in float32 and the 32 lane partials of a row are reduced with the
+// transposed float32 butterfly (32 rows per warp iteration, ~4 instructions per row). Slices
+// are chained through a float64 partial per row (8 B/row per extra slice, +3% traffic for
+// 2048-bit codes). Every row is summed in the same fixed order (position independent).
+constexpr int kBinThreads = 512;
 
-// Fast path: row bytes == 16 * CH (CH chunks of 16 bytes, CH % 16 == 0), R rows per group
-// per iteration; 2 groups (half-warps) per warp. The nibble tables are built per CTA from w.
-template <int CH, int R>
-__global__ void __launch_bounds__(256) bin_score_fast(const uint8_t* __restrict__ codes, int64_t n,
-                                                      const double* __restrict__ w, int n_bits,
-                                                      float* __restrict__ out,
-                                                      uint32_t* __restrict__ ghist) {
-  constexpr int TPL = CH / 16;  // chunks per lane
-  extern __shared__ double lut[];  // CH*32*16 doubles
+template <int RB>  // row bytes (compile-time so per-row offsets are immediates)
+__global__ void __launch_bounds__(kBinThreads, 1)
+bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
+                const double* __restrict__ w, int n_bits, const double* __restrict__ partial_in,
+                double* __restrict__ partial_out, float* __restrict__ out,
+                uint32_t* __restrict__ ghist) {
+  extern __shared__ __align__(16) unsigned char tabb[];  // 128 KB
   __shared__ uint32_t sh[kHistBins];
-  for (int e = threadIdx.x; e < CH * 32 * 16; e += blockDim.x) {
-    int slot;
-    const double v = nibble_entry(w, n_bits, e, &slot);
-    lut[slot] = v;
+  for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
+    const int l = e & 31, k = (e >> 5) & 3, v = e >> 7;  // consecutive threads -> consecutive banks
+    const int bit0 = 8 * (slice * 128 + 4 * l + k);
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if ((v >> b) & 1) s = __dadd_rn(s, bit0 + b < n_bits ? (double)__double2float_rn(w[bit0 + b]) : 0.0);
+    const uint32_t addr = ((uint32_t)(k >> 1) << 16) | ((uint32_t)v << 8) | ((uint32_t)(k & 1) << 7) | ((uint32_t)l << 2);
+    *reinterpret_cast<float*>(tabb + addr) = __double2float_rn(s);
   }
-  if (ghist) hist_zero(sh);
+  if (ghist && out) hist_zero(sh);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int cl = lane & 15;    // chunk lane
-  const int grp = lane >> 4;   // row group within the warp
+  // per-lane constant bytes: [l<<2, l<<2 | 0x80, 0, 1]
+  const uint32_t L = ((uint32_t)lane << 2) | (((uint32_t)lane << 2 | 0x80u) << 8) | (1u << 24);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint4* C4 = reinterpret_cast<const uint4*>(codes);
-  for (int64_t r0 = warp * (2 * R); r0 < n; r0 += nwarp * (2 * R)) {
-    uint4 v[R][TPL];
+  const uint8_t* base = codes + (int64_t)slice * 128 + 4 * lane;
+  constexpr int R = 32;  // rows per warp iteration
+  for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
+    uint32_t wd[R];
+    const uint8_t* rp = base + r0 * RB;
+    if (r0 + R <= n) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) wd[i] = __ldcs(reinterpret_cast<const uint32_t*>(rp + i * RB));
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        wd[i] = r0 + i < n ? __ldcs(reinterpret_cast<const uint32_t*>(rp + i * RB)) : 0u;
+    }
+    float p[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const int64_t row = r0 + grp * R + i;
-#pragma unroll
-      for (int t = 0; t < TPL; ++t) {
-        if (row < n) v[i][t] = ld_stream_u4(C4 + row * CH + cl + 16 * t);
-        else v[i][t] = make_uint4(0, 0, 0, 0);
-      }
+      const uint32_t x = wd[i];
+      float s = *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6604));
+      s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6615)));
+      s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6724)));
+      s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6735)));
+      p[i] = s;
     }
-    double p[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t < TPL; ++t) {
-        const uint32_t words[4] = {v[i][t].x, v[i][t].y, v[i][t].z, v[i][t].w};
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const uint32_t nib = (words[q >> 3] >> (4 * (q & 7))) & 15u;
-          acc = __dadd_rn(acc, lut[((t * 32 + q) * 16 + nib) * 16 + cl]);
-        }
-      }
-      p[i] = acc;
-    }
-    transposed_reduce<R, 16>(p, lane);
+    transposed_reduce_f<R, 32>(p, lane);
     bool writer;
-    const int slot = row_of_lane<R, 16>(lane, &writer);
-    const int64_t row = r0 + grp * R + slot;
+    const int slot = row_of_lane<R, 32>(lane, &writer);
+    const int64_t row = r0 + slot;
     const bool active = writer && row < n;
-    const float s = __double2float_rn(p[0]);
-    if (active) out[row] = s;
-    if (ghist) hist_add(sh, active, hist_bin(s));
+    double total = (double)p[0];
+    if (active && partial_in) total = __dadd_rn(__ldcs(partial_in + row), total);
+    if (out) {
+      const float sc = __double2float_rn(total);
+      if (active) out[row] = sc;
+      if (ghist) hist_add(sh, active, hist_bin(sc));
+    } else if (active) {
+      partial_out[row] = total;
+    }
   }
-  if (ghist) {
+  if (ghist && out) {
     __syncthreads();
     hist_flush(sh, ghist);
   }
@@ -191,42 +187,46 @@ __global__ void bin_hamming(const uint8_t* __restrict__ a, const uint8_t* __rest
   }
 }
 
-size_t bin_lut_bytes(int n_bits) {
+// fast path when rows are whole 128-byte slices; scratch: n doubles when slices > 1
+bool bin_bytes_path(int n_bits, const uint8_t* codes) {
   const int row_bytes = (n_bits + 7) / 8;
-  if (row_bytes % 256 != 0 || row_bytes > 512) return 0;  // fast path: CH in {16, 32}
-  return (size_t)(row_bytes / 16) * 32 * 16 * sizeof(double);
-}
-
-template <int CH, int R>
-static int launch_fast(const uint8_t* codes, int64_t n, const double* w, int n_bits, float* out,
-                       uint32_t* hist, int device, cudaStream_t st) {
-  auto fn = bin_score_fast<CH, R>;
-  const size_t smem = (size_t)CH * 32 * 16 * sizeof(double);
-  static bool configured[64] = {false};
-  if (!configured[device & 63]) {
-    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured[device & 63] = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)per_sm * sm_count(device);
-  const int64_t need = (n + 16 * R - 1) / (16 * R);
-  if (need < grid) grid = need;
-  fn<<<(int)grid, 256, smem, st>>>(codes, n, w, n_bits, out, hist);
-  OTF_LAUNCH_CHECK("bin_score_fast");
-  return OTF_OK;
+  return n_bits % 8 == 0 && (row_bytes == 128 || row_bytes == 256 || row_bytes == 512 || row_bytes == 1024) &&
+         (((uintptr_t)codes) & 3) == 0;
 }
 
 // w: float64 model (device); cast to float32 in-kernel (ranker.py:89). hist: see dense.
 int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
-                     uint32_t* hist, int device, cudaStream_t st) {
+                     uint32_t* hist, double* scratch, int device, cudaStream_t st) {
   if (n <= 0) return OTF_OK;
   const int row_bytes = (n_bits + 7) / 8;
-  const bool aligned = (((uintptr_t)codes) & 15) == 0;
-  if (aligned && bin_lut_bytes(n_bits) > 0) {
-    if (row_bytes == 256) return launch_fast<16, 8>(codes, n, w, n_bits, out, hist, device, st);
-    if (row_bytes == 512) return launch_fast<32, 4>(codes, n, w, n_bits, out, hist, device, st);
+  if (bin_bytes_path(n_bits, codes) && (row_bytes == 128 || scratch != nullptr)) {
+    const int slices = row_bytes / 128;
+    const size_t smem = (size_t)4 * 256 * 32 * sizeof(float);
+    static bool configured[64] = {false};
+    if (!configured[device & 63]) {
+      cudaFuncSetAttribute((const void*)bin_score_bytes<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured[device & 63] = true;
+    }
+    int64_t grid = sm_count(device);  // one 512-thread CTA per SM (128 KB table)
+    const int64_t need = (n + (kBinThreads / 32) * 32 - 1) / ((kBinThreads / 32) * 32);
+    if (need < grid) grid = need;
+    for (int s = 0; s < slices; ++s) {
+      const bool last = s == slices - 1;
+      const double* pin = s ? scratch : nullptr;
+      double* pout = last ? nullptr : scratch;
+      float* o = last ? out : nullptr;
+      switch (row_bytes) {
+        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
+        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
+        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
+        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
+      }
+      OTF_LAUNCH_CHECK("bin_score_bytes");
+    }
+    return OTF_OK;
   }
   int64_t grid = (n + 7) / 8;
   const int64_t cap = 8LL * sm_count(device);

@@ -242,8 +242,11 @@ int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStr
     return launch_pq_scan(codes, r->n, r->M, nullptr, nullptr, static_cast<const double*>(r->lut.p),
                           r->K, r->Q, static_cast<double*>(out), hist, r->device, st);
   }
+  // multi-slice byte-table path chains a float64 partial per row
+  if ((rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(double)))) return rc;
   return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, dw,
-                          static_cast<float*>(out), hist, r->device, st);
+                          static_cast<float*>(out), hist, static_cast<double*>(r->bins.p), r->device,
+                          st);
 }
 
 int score_dtype(const otf_repo* r) { return r->kind == OTF_KIND_PQ ? OTF_F64 : OTF_F32; }
@@ -491,11 +494,9 @@ int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* id
     const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
     int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
     if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
-    if (!rc) rc = r->w32.ensure((size_t)r->model_dim * sizeof(float));
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
-    if (!rc && (r->kind == OTF_KIND_BINARY) && bin_lut_bytes(r->model_dim))
-      rc = r->lut.ensure(bin_lut_bytes(r->model_dim));
+    if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
     if (rc) return rc;
     cudaStream_t cap;
     OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -627,9 +628,14 @@ int otf_score_binary(int device, const uint8_t* codes, int64_t n, int32_t output
   if ((rc = S.in(codes, (size_t)n * row_bytes, mem, &dc))) return rc;
   if ((rc = S.in(w, (size_t)output_bits * 8, mem, &dw))) return rc;
   if ((rc = S.outbuf(out, (size_t)n * 4, mem, &dout))) return rc;
-  if ((rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<const double*>(dw),
-                             static_cast<float*>(dout), nullptr, device, st))) return rc;
-  return S.out(out, dout, (size_t)n * 4, mem);
+  DevBuf scratch;
+  if ((rc = scratch.ensure((size_t)(n > 0 ? n : 1) * sizeof(double)))) return rc;
+  rc = launch_bin_score(static_cast<const uint8_t*>(dc), n, output_bits, static_cast<const double*>(dw),
+                        static_cast<float*>(dout), nullptr, static_cast<double*>(scratch.p), device, st);
+  if (!rc) rc = S.out(out, dout, (size_t)n * 4, mem);
+  cudaStreamSynchronize(st);  // scratch is freed on return
+  scratch.release();
+  return rc;
 }
 
 int otf_unpack_bits(int device, const uint8_t* codes, int64_t n, int32_t output_bits, float* out,

@@ -120,6 +120,29 @@ __device__ __forceinline__ void transposed_reduce(double (&p)[R], int lane) {
     }
   }
 }
+// float32 variant (same tree).
+template <int R, int LPR>
+__device__ __forceinline__ void transposed_reduce_f(float (&p)[R], int lane) {
+  int count = R;
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) {
+    if (count > 1) {
+      const int half = count >> 1;
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < R / 2; ++j) {
+        if (j < half) {
+          const float send = upper ? p[j] : p[j + half];
+          const float keep = upper ? p[j + half] : p[j];
+          p[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+        }
+      }
+      count = half;
+    } else {
+      p[0] = __fadd_rn(p[0], __shfl_xor_sync(0xffffffffu, p[0], o));
+    }
+  }
+}
 // Row slot (0..R-1) that lane `lane` holds after transposed_reduce<R, LPR>, and whether it
 // is the designated writer for that row.
 template <int R, int LPR>

@@ -28,9 +28,11 @@ int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, c
                    cudaStream_t st);
 
 // binary (otf_binary.cu)
-size_t bin_lut_bytes(int n_bits);
+// byte-table fast path for rows of whole 128-byte slices; needs `scratch` (n doubles) when a
+// row has more than one slice (> 1024 bits); otherwise the generic kernel runs.
+bool bin_bytes_path(int n_bits, const uint8_t* codes);
 int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
-                     uint32_t* hist, int device, cudaStream_t st);
+                     uint32_t* hist, double* scratch, int device, cudaStream_t st);
 int launch_bin_unpack(const uint8_t* codes, int64_t n, int n_bits, float* out, int device,
                       cudaStream_t st);
 int launch_binarize(const double* U, const float* mu, int m, int n_bits, const double* X,
