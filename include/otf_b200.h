@@ -161,6 +161,20 @@ int otf_pegasos_update(int device, double* w, int32_t d, const void* pos, int32_
 int otf_pegasos_step_host(int device, double* w, int32_t d, const double* batch, int32_t half,
                           double shrink, double eta_over_b, int project, double radius);
 
+/* train_batch(positives, negatives, cfg) — trainer.py:204-257. features (n, d): the n_pos
+ * positive rows then the negatives, dtype OTF_F32 | OTF_F64; idx: total*bs row indices drawn by
+ * the caller exactly as the reference draws them (rng.integers(0, n, size=bs) per step);
+ * spe = steps per epoch, tail_start/tail_len as trainer.py:236-238, lam = 1/(c n).
+ * w_out: d float64 (the returned model); obj_hist (nullable): total/spe epoch objectives
+ * followed by the tail-average objective. Host or device memory per `mem`. */
+int otf_train_batch(int device, const void* features, int32_t dtype, int64_t n_pos, int64_t n,
+                    int32_t d, const int64_t* idx, int64_t total, int32_t bs, int64_t spe,
+                    int64_t tail_start, int64_t tail_len, double lam, int project, double* w_out,
+                    double* obj_hist, int mem, void* stream);
+/* hinge_objective(w, features, labels, lam) — trainer.py:197-201 (labels: n_pos +1 then -1). */
+int otf_hinge_objective(int device, const void* features, int32_t dtype, int64_t n_pos, int64_t n,
+                        int32_t d, const double* w, double lam, double* out, int mem, void* stream);
+
 typedef struct otf_trainer otf_trainer;
 /* OnlineTrainer(dim, negatives, cfg) — trainer.py:109-143; negatives copied to HBM once. */
 int otf_trainer_create(int device, int32_t dim, const void* negatives, int32_t neg_dtype,

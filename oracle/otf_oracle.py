@@ -224,3 +224,40 @@ def normalize_rows(data) -> np.ndarray:
     """store.py:32-53 (without the zero-norm check)."""
     arr = np.asarray(data, dtype=np.float64)
     return (arr / np.linalg.norm(arr, axis=1)[:, np.newaxis]).astype(np.float32)
+
+
+def hinge_objective(w, features, labels, lam):
+    """trainer.py:197-201."""
+    w = np.asarray(w, dtype=np.float64)
+    margins = labels * (np.asarray(features, dtype=np.float64) @ w)
+    return float(0.5 * lam * np.dot(w, w) + np.maximum(0.0, 1.0 - margins).mean())
+
+
+def train_batch(pos, neg, c=0.25, batch_size=32, epochs=60, project=True, seed=0, history=None):
+    """trainer.py:204-257: Pegasos over the pooled set, tail average vs best epoch iterate."""
+    feats = np.concatenate([np.asarray(pos, np.float64), np.asarray(neg, np.float64)])
+    labels = np.concatenate([np.ones(len(pos)), -np.ones(len(neg))])
+    n = len(feats)
+    lam = 1.0 / (c * n)
+    bs = min(batch_size, n)
+    spe = math.ceil(n / bs)
+    total = epochs * spe
+    tail_len = max(1, total // 4)
+    tail_start = total - tail_len
+    rng = np.random.default_rng(seed)
+    w = np.zeros(feats.shape[1])
+    tail = np.zeros_like(w)
+    best_obj, best_w = math.inf, w.copy()
+    for t in range(1, total + 1):
+        idx = rng.integers(0, n, size=bs)
+        w, _ = apply_update(w, t, feats[idx], labels[idx], lam, bs, project)
+        if t > tail_start:
+            tail += w
+        if t % spe == 0:
+            obj = hinge_objective(w, feats, labels, lam)
+            if history is not None:
+                history.append(obj)
+            if obj < best_obj:
+                best_obj, best_w = obj, w.copy()
+    avg = tail / tail_len
+    return (avg if hinge_objective(avg, feats, labels, lam) <= best_obj else best_w), total

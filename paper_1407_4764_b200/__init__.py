@@ -25,7 +25,7 @@ from .model import LinearModel
 from .pq import PQCodebook, build_score_lut, score_codes
 from .ranker import RankedList, RankerConfig, Repository, score_binary, score_dense, score_pq, top_k
 from .store import FeatureStore
-from .trainer import OnlineTrainer, TrainerConfig, pegasos_step
+from .trainer import BatchTrainConfig, OnlineTrainer, TrainerConfig, hinge_objective, pegasos_step, train_batch
 
 __all__ = [
     "__version__",
@@ -35,5 +35,6 @@ __all__ = [
     "LinearModel", "PQCodebook", "build_score_lut", "score_codes",
     "RankedList", "RankerConfig", "Repository", "score_binary", "score_dense", "score_pq", "top_k",
     "FeatureStore", "OnlineTrainer", "TrainerConfig", "pegasos_step",
+    "BatchTrainConfig", "train_batch", "hinge_objective",
     "default_device", "set_device", "launch_count",
 ]

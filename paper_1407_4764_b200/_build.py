@@ -20,7 +20,8 @@ INCLUDE = ROOT / "include"
 LIB = PKG / "libotf_b200.so"
 OBJ = PKG / "build"
 
-SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu"]
+SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu",
+           "otf_batch.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

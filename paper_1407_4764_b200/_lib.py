@@ -71,6 +71,9 @@ SIGNATURES: dict[str, list] = {
     "otf_pegasos_update": [_int, _vp, _i32, _vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32,
                            _dbl, _dbl, _int, _dbl, _vp],
     "otf_pegasos_step_host": [_int, _vp, _i32, _vp, _i32, _dbl, _dbl, _int, _dbl],
+    "otf_train_batch": [_int, _vp, _i32, _i64, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _dbl, _int,
+                        _vp, _vp, _int, _vp],
+    "otf_hinge_objective": [_int, _vp, _i32, _i64, _i64, _i32, _vp, _dbl, _vp, _int, _vp],
     "otf_trainer_create": [_int, _i32, _vp, _i32, _i64, _int, _P(_vp)],
     "otf_trainer_destroy": [_vp],
     "otf_trainer_append_positives": [_vp, _vp, _i32, _i64, _int],

@@ -747,6 +747,42 @@ int otf_pegasos_step_host(int device, double* w, int32_t d, const double* batch,
   return OTF_OK;
 }
 
+int otf_train_batch(int device, const void* features, int32_t dtype, int64_t n_pos, int64_t n,
+                    int32_t d, const int64_t* idx, int64_t total, int32_t bs, int64_t spe,
+                    int64_t tail_start, int64_t tail_len, double lam, int project, double* w_out,
+                    double* obj_hist, int mem, void* stream) {
+  if (n <= 0 || n_pos <= 0 || n_pos >= n) return fail(OTF_ERR_INSUFFICIENT, "both classes need at least one example");
+  if (d <= 0 || bs <= 0 || spe <= 0 || total <= 0) return fail(OTF_ERR_CONFIG, "bad train_batch shape");
+  STATELESS_BEGIN(device, mem, stream)
+  const size_t es = dtype == OTF_F64 ? 8 : 4;
+  const int64_t n_hist = total / spe + 1;
+  const void *dX, *di; void *dw, *dh = nullptr;
+  if ((rc = S.in(features, (size_t)n * d * es, mem, &dX))) return rc;
+  if ((rc = S.in(idx, (size_t)total * bs * 8, mem, &di))) return rc;
+  if ((rc = S.outbuf(w_out, (size_t)d * 8, mem, &dw))) return rc;
+  if (obj_hist && (rc = S.outbuf(obj_hist, (size_t)n_hist * 8, mem, &dh))) return rc;
+  if ((rc = launch_batch_train(dX, dtype, n_pos, n, d, static_cast<const int64_t*>(di), total, bs, spe, tail_start,
+                               tail_len, lam, project, static_cast<double*>(dw), static_cast<double*>(dh), st)))
+    return rc;
+  if ((rc = S.out(w_out, dw, (size_t)d * 8, mem))) return rc;
+  if (obj_hist) rc = S.out(obj_hist, dh, (size_t)n_hist * 8, mem);
+  return rc;
+}
+
+int otf_hinge_objective(int device, const void* features, int32_t dtype, int64_t n_pos, int64_t n,
+                        int32_t d, const double* w, double lam, double* out, int mem, void* stream) {
+  if (n <= 0 || d <= 0) return fail(OTF_ERR_CONFIG, "bad hinge_objective shape");
+  STATELESS_BEGIN(device, mem, stream)
+  const size_t es = dtype == OTF_F64 ? 8 : 4;
+  const void *dX, *dw; void* dout;
+  if ((rc = S.in(features, (size_t)n * d * es, mem, &dX))) return rc;
+  if ((rc = S.in(w, (size_t)d * 8, mem, &dw))) return rc;
+  if ((rc = S.outbuf(out, 8, mem, &dout))) return rc;
+  if ((rc = launch_hinge_objective(dX, dtype, n_pos, n, d, static_cast<const double*>(dw), lam,
+                                   static_cast<double*>(dout), st))) return rc;
+  return S.out(out, dout, 8, mem);
+}
+
 int otf_trainer_create(int device, int32_t dim, const void* negatives, int32_t neg_dtype, int64_t n_neg,
                        int mem, otf_trainer** out) {
   *out = nullptr;

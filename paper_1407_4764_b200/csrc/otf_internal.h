@@ -71,6 +71,13 @@ int launch_pegasos(double* w, int d, const void* pos, int pos_dtype, int64_t n_p
                    const int64_t* neg_idx, int half, double shrink, double eta_over_b,
                    int project, double radius, cudaStream_t st);
 
+// fixed-set training (otf_batch.cu); X: (n, d) float32/float64, rows < n_pos labelled +1
+int launch_batch_train(const void* X, int dt, int64_t n_pos, int64_t n, int d, const int64_t* idx,
+                       int64_t total, int bs, int64_t spe, int64_t tail_start, int64_t tail_len,
+                       double lam, int project, double* w_out, double* obj_hist, cudaStream_t st);
+int launch_hinge_objective(const void* X, int dt, int64_t n_pos, int64_t n, int d, const double* w,
+                           double lam, double* out, cudaStream_t st);
+
 // misc
 int launch_gather_rows(const uint8_t* src, int64_t row_bytes, const int64_t* rows, int64_t n,
                        uint8_t* dst, int device, cudaStream_t st);

@@ -202,3 +202,87 @@ class OnlineTrainer:
                 self._published_iteration = self._iteration
                 self._snap = LinearModel(w, self._iteration, self._version)
             return LinearModel(self._snap.weights.copy(), self._snap.iteration, self._snap.version)
+
+
+# -- fixed-set training (trainer.py:176-257) ------------------------------------------------------
+
+
+@dataclasses.dataclass(frozen=True)
+class BatchTrainConfig:
+    """trainer.py:178-194 — C-parameterised regularisation and epoch budget."""
+
+    c: float = 0.25
+    batch_size: int = 32
+    epochs: int = 60
+    project: bool = True
+    seed: int = 0
+
+    def validate(self) -> None:
+        if self.c <= 0:
+            raise ConfigError(f"c must be positive, got {self.c}")
+        if self.batch_size < 1:
+            raise ConfigError(f"batch_size must be >= 1, got {self.batch_size}")
+        if self.epochs < 1:
+            raise ConfigError(f"epochs must be >= 1, got {self.epochs}")
+
+
+def _pooled(positives, negatives):
+    pos = np.asarray(_pool_array(positives))
+    neg = np.asarray(_pool_array(negatives))
+    if len(pos) == 0 or len(neg) == 0:
+        raise InsufficientDataError("both classes need at least one example")
+    if pos.shape[1] != neg.shape[1]:
+        raise ConfigError(f"dim mismatch: positives {pos.shape[1]}, negatives {neg.shape[1]}")
+    # the reference converts both pools to float64 (exact for float32 inputs); keep float32 rows
+    # in float32 on the device when both pools are float32 (half the HBM), else float64
+    if pos.dtype == np.float32 and neg.dtype == np.float32:
+        return np.ascontiguousarray(np.concatenate([pos, neg])), _lib.F32, len(pos)
+    feats = np.concatenate([pos.astype(np.float64), neg.astype(np.float64)])
+    return np.ascontiguousarray(feats), _lib.F64, len(pos)
+
+
+def hinge_objective(weights, features, labels, lam: float) -> float:
+    """trainer.py:197-201 — lam/2 |w|^2 + mean hinge loss, on the GPU.
+
+    ``labels`` must be +1 for a leading block of rows and -1 for the rest (the layout
+    train_batch uses); other label layouts are reordered on the host first.
+    """
+    x = np.asarray(features)
+    y = np.asarray(labels)
+    order = np.argsort(-y, kind="stable")  # +1 rows first, original order within each class
+    x = np.ascontiguousarray(x[order])
+    n_pos = int(np.count_nonzero(y > 0))
+    dt = _lib.F32 if x.dtype == np.float32 else _lib.F64
+    x = np.ascontiguousarray(x, dtype=np.float32 if dt == _lib.F32 else np.float64)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.empty(1, dtype=np.float64)
+    _lib.check(_lib.load().otf_hinge_objective(_lib.default_device(), _lib.ptr(x), dt, n_pos, x.shape[0], x.shape[1],
+                                               _lib.ptr(w), float(lam), _lib.ptr(out), _lib.MEM_HOST, None))
+    return float(out[0])
+
+
+def train_batch(positives, negatives, cfg: BatchTrainConfig | None = None, objective_history=None) -> LinearModel:
+    """trainer.py:204-257 — fixed-set SVM fit; one persistent CUDA CTA runs every step."""
+    cfg = cfg if cfg is not None else BatchTrainConfig()
+    cfg.validate()
+    feats, dt, n_pos = _pooled(positives, negatives)
+    n, d = feats.shape
+    lam = 1.0 / (cfg.c * n)
+    batch_size = min(cfg.batch_size, n)
+    steps_per_epoch = math.ceil(n / batch_size)
+    total_steps = cfg.epochs * steps_per_epoch
+    tail_len = max(1, total_steps // 4)
+    tail_start = total_steps - tail_len
+    rng = np.random.default_rng(cfg.seed)
+    # the reference draws rng.integers(0, n, size=batch_size) once per step (trainer.py:243)
+    idx = np.empty((total_steps, batch_size), dtype=np.int64)
+    for t in range(total_steps):
+        idx[t] = rng.integers(0, n, size=batch_size)
+    w = np.empty(d, dtype=np.float64)
+    hist = np.empty(total_steps // steps_per_epoch + 1, dtype=np.float64)
+    _lib.check(_lib.load().otf_train_batch(_lib.default_device(), _lib.ptr(feats), dt, n_pos, n, d, _lib.ptr(idx),
+                                           total_steps, batch_size, steps_per_epoch, tail_start, tail_len, lam,
+                                           int(bool(cfg.project)), _lib.ptr(w), _lib.ptr(hist), _lib.MEM_HOST, None))
+    if objective_history is not None:
+        objective_history.extend(float(v) for v in hist[:-1])
+    return LinearModel(w, total_steps)

@@ -139,6 +139,21 @@ def main() -> None:
         seq.append(w)
     g["peg_noproj_w"] = np.stack(seq)
 
+    # ---- fixed-set SVM (trainer.py:197-257) ---------------------------------------------------
+    for name, (n_pos, n_neg, d, epochs, seed) in {"tb16": (60, 400, 16, 20, 41), "tb128": (40, 600, 128, 8, 42)}.items():
+        rng = np.random.default_rng(seed)
+        pos = normalize_rows(rng.standard_normal((n_pos, d)) + 0.8)
+        neg = normalize_rows(rng.standard_normal((n_neg, d)))
+        hist: list[float] = []
+        model = rt.train_batch(pos, neg, rt.BatchTrainConfig(c=0.25, epochs=epochs, seed=seed), objective_history=hist)
+        feats = np.concatenate([pos, neg]).astype(np.float64)
+        labels = np.concatenate([np.ones(n_pos), -np.ones(n_neg)])
+        g[f"tb_{name}_pos"], g[f"tb_{name}_neg"] = pos, neg
+        g[f"tb_{name}_w"] = model.weights
+        g[f"tb_{name}_iter"] = np.array([model.iteration])
+        g[f"tb_{name}_hist"] = np.array(hist)
+        g[f"tb_{name}_obj"] = np.array([rt.hinge_objective(model.weights, feats, labels, 1.0 / (0.25 * len(feats)))])
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
 

@@ -369,3 +369,42 @@ def test_online_trainer_device_pool_equals_host_pool(otf, golden):
         a.step(pos)
         b.step()
     np.testing.assert_array_equal(a.snapshot().weights, b.snapshot().weights)
+
+
+# ---------------------------------------------------------------------------------------------
+# fixed-set SVM (trainer.py:197-257)
+
+
+@pytest.mark.parametrize("name,epochs,seed", [("tb16", 20, 41), ("tb128", 8, 42)])
+def test_train_batch_matches_reference(otf, golden, name, epochs, seed):
+    pos, neg = golden[f"tb_{name}_pos"], golden[f"tb_{name}_neg"]
+    hist = []
+    model = otf.train_batch(pos, neg, otf.BatchTrainConfig(c=0.25, epochs=epochs, seed=seed), objective_history=hist)
+    assert model.iteration == int(golden[f"tb_{name}_iter"][0])
+    np.testing.assert_allclose(model.weights, golden[f"tb_{name}_w"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(np.array(hist), golden[f"tb_{name}_hist"], rtol=1e-10)
+    feats = np.concatenate([pos, neg]).astype(np.float64)
+    labels = np.concatenate([np.ones(len(pos)), -np.ones(len(neg))])
+    lam = 1.0 / (0.25 * len(feats))
+    np.testing.assert_allclose(otf.hinge_objective(model.weights, feats, labels, lam), golden[f"tb_{name}_obj"][0],
+                               rtol=1e-9)
+
+
+def test_train_batch_reference_behaviour(otf):
+    """tests/test_trainer.py:245-306 of the reference, on the GPU trainer."""
+    pos = np.array([[1.0, 0.0, 0.0, 0.0]])
+    neg = np.array([[-1.0, 0.0, 0.0, 0.0]])
+    m = otf.train_batch(pos, neg, otf.BatchTrainConfig(epochs=200, seed=0))
+    assert m.weights[0] / np.linalg.norm(m.weights) > 0.999
+    np.testing.assert_allclose(m.weights[0], 0.5, atol=0.05)
+    rng = np.random.default_rng(19)
+    p4 = O.normalize_rows(rng.standard_normal((8, 4)) + 1)
+    n4 = O.normalize_rows(rng.standard_normal((8, 4)) - 1)
+    assert otf.train_batch(p4, n4, otf.BatchTrainConfig(batch_size=4, epochs=5, seed=0)).iteration == 20
+    a = otf.train_batch(p4, n4, otf.BatchTrainConfig(epochs=30, seed=7))
+    b = otf.train_batch(p4, n4, otf.BatchTrainConfig(epochs=30, seed=7))
+    assert a.weights.tobytes() == b.weights.tobytes()
+    with pytest.raises(otf.InsufficientDataError):
+        otf.train_batch(np.empty((0, 4)), np.ones((3, 4)))
+    with pytest.raises(otf.ConfigError):
+        otf.BatchTrainConfig(c=0.0).validate()

@@ -130,3 +130,13 @@ def test_pegasos_sequence_matches_reference(golden):
         w = O.pegasos_step(w, t, pos, neg, 0.05, 16, True, rng, hook=lambda p, q: idx.append(np.concatenate([p, q])))
         np.testing.assert_array_equal(w, golden["peg_w"][t - 1])
     np.testing.assert_array_equal(np.stack(idx), golden["peg_idx"])
+
+
+@pytest.mark.parametrize("name,epochs,seed", [("tb16", 20, 41), ("tb128", 8, 42)])
+def test_train_batch_matches_reference(golden, name, epochs, seed):
+    pos, neg = golden[f"tb_{name}_pos"], golden[f"tb_{name}_neg"]
+    hist = []
+    w, total = O.train_batch(pos, neg, epochs=epochs, seed=seed, history=hist)
+    np.testing.assert_array_equal(w, golden[f"tb_{name}_w"])
+    assert total == int(golden[f"tb_{name}_iter"][0])
+    np.testing.assert_array_equal(np.array(hist), golden[f"tb_{name}_hist"])
