@@ -105,6 +105,16 @@ int otf_repo_rank(otf_repo* repo, const double* w, int64_t k, int64_t* out_ids,
                   double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
                   void* stream);
 
+/* Many classifiers over one dense repository (C5b; no single reference call — the reference
+ * needs n_cls separate score_dense calls, ranker.py:63-69). W: (n_cls, model_dim) float64.
+ * Scores on the tcgen05 tensor cores in TF32 with a 3-product split (float32-level accuracy);
+ * requires model_dim % 32 == 0. out: (n_cls, count) float32, classifier-major. */
+int otf_repo_score_many(otf_repo* repo, const double* W, int32_t n_cls, float* out, int mem,
+                        void* stream);
+/* ... and the exact top-k of each classifier: out_ids / out_scores (n_cls, n_out). */
+int otf_repo_rank_many(otf_repo* repo, const double* W, int32_t n_cls, int64_t k, int64_t* out_ids,
+                       double* out_scores, int64_t* out_n, int mem, void* stream);
+
 /* Capture repo's rank(k) for a device-resident w into a CUDA graph and replay it
  * (the live ranker re-ranks every tau with a new w in the same buffer). Device memory only. */
 int otf_repo_rank_graph(otf_repo* repo, const double* w_dev, int64_t k, int64_t* ids_dev,

@@ -20,7 +20,7 @@ INCLUDE = ROOT / "include"
 LIB = PKG / "libotf_b200.so"
 OBJ = PKG / "build"
 
-SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu",
+SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu", "otf_multi.cu",
            "otf_batch.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -60,6 +60,8 @@ SIGNATURES: dict[str, list] = {
     "otf_repo_score": [_vp, _vp, _vp, _int, _vp],
     "otf_repo_rank": [_vp, _vp, _i64, _vp, _vp, _vp, _P(_i64), _int, _vp],
     "otf_repo_rank_graph": [_vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "otf_repo_score_many": [_vp, _vp, _i32, _vp, _int, _vp],
+    "otf_repo_rank_many": [_vp, _vp, _i32, _i64, _vp, _vp, _P(_i64), _int, _vp],
     "otf_score_dense": [_int, _vp, _i64, _i32, _vp, _vp, _int, _vp],
     "otf_pq_build_lut": [_int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp],
     "otf_pq_score_codes": [_int, _vp, _i32, _i32, _vp, _i64, _vp, _int, _vp],

@@ -478,6 +478,93 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
   return OTF_OK;
 }
 
+// ---- many classifiers (C5b): tensor-core scoring of a dense repository ----------------------------
+namespace {
+// scores for classifiers [c0, c0 + cn) into out (cn x n float32, classifier-major); W host/device.
+int multi_score_group(otf_repo* r, const double* dW, int cn, float* out, cudaStream_t st) {
+  int rc = r->w32.ensure((size_t)2 * 64 * r->model_dim * sizeof(float));
+  if (rc) return rc;
+  return launch_multi_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dW, cn,
+                            static_cast<float*>(r->w32.p), out, r->device, st);
+}
+}  // namespace
+
+int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out, int mem, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  if (r->kind != OTF_KIND_DENSE) return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs a dense repository");
+  if (n_cls < 1) return fail(OTF_ERR_CONFIG, "n_cls must be positive");
+  if (!multi_tc_supported(r->model_dim, static_cast<const float*>(r->payload)))
+    return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs dim % 32 == 0");
+  cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
+  const size_t wbytes = (size_t)n_cls * r->model_dim * sizeof(double);
+  DevBuf dW, dOut;
+  const double* wp = W;
+  int rc = OTF_OK;
+  if (mem == OTF_MEM_HOST) {
+    if ((rc = dW.ensure(wbytes))) return rc;
+    OTF_CUDA(cudaMemcpyAsync(dW.p, W, wbytes, cudaMemcpyHostToDevice, st));
+    wp = static_cast<const double*>(dW.p);
+    if ((rc = dOut.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
+  }
+  for (int c0 = 0; c0 < n_cls && !rc; c0 += 64) {
+    const int cn = std::min(64, n_cls - c0);
+    float* o = mem == OTF_MEM_HOST ? static_cast<float*>(dOut.p) : out + (size_t)c0 * r->n;
+    rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, o, st);
+    if (!rc && mem == OTF_MEM_HOST) {
+      cudaError_t e = cudaMemcpyAsync(out + (size_t)c0 * r->n, o, (size_t)cn * r->n * sizeof(float),
+                                      cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
+    }
+  }
+  if (mem == OTF_MEM_HOST || rc) cudaStreamSynchronize(st);
+  dW.release(); dOut.release();
+  return rc;
+}
+
+int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, int64_t* out_ids,
+                       double* out_scores, int64_t* out_n, int mem, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  if (r->kind != OTF_KIND_DENSE) return fail(OTF_ERR_CONFIG, "multi-classifier ranking needs a dense repository");
+  if (n_cls < 1) return fail(OTF_ERR_CONFIG, "n_cls must be positive");
+  if (!multi_tc_supported(r->model_dim, static_cast<const float*>(r->payload)))
+    return fail(OTF_ERR_CONFIG, "multi-classifier ranking needs dim % 32 == 0");
+  const int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  if (out_n) *out_n = k_eff;
+  if (k_eff == 0) return OTF_OK;
+  cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
+  const size_t wbytes = (size_t)n_cls * r->model_dim * sizeof(double);
+  DevBuf dW, dIds, dSc, scores;
+  const double* wp = W;
+  int rc = OTF_OK;
+  if (mem == OTF_MEM_HOST) {
+    if ((rc = dW.ensure(wbytes))) return rc;
+    OTF_CUDA(cudaMemcpyAsync(dW.p, W, wbytes, cudaMemcpyHostToDevice, st));
+    wp = static_cast<const double*>(dW.p);
+    if ((rc = dIds.ensure((size_t)n_cls * k_eff * 8)) || (rc = dSc.ensure((size_t)n_cls * k_eff * 8))) return rc;
+  }
+  int64_t* ids = mem == OTF_MEM_HOST ? static_cast<int64_t*>(dIds.p) : out_ids;
+  double* sc = mem == OTF_MEM_HOST ? static_cast<double*>(dSc.p) : out_scores;
+  if ((rc = scores.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
+  for (int c0 = 0; c0 < n_cls && !rc; c0 += 64) {
+    const int cn = std::min(64, n_cls - c0);
+    rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, static_cast<float*>(scores.p), st);
+    for (int c = 0; c < cn && !rc; ++c)
+      rc = launch_topk(static_cast<const float*>(scores.p) + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base,
+                       k_eff, &r->topk, false, ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff,
+                       nullptr, r->device, st);
+  }
+  if (!rc && mem == OTF_MEM_HOST) {
+    cudaError_t e = cudaMemcpyAsync(out_ids, ids, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_scores, sc, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
+  }
+  cudaStreamSynchronize(st);  // the score buffer is released on return
+  dW.release(); dIds.release(); dSc.release(); scores.release();
+  return rc;
+}
+
 int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* ids_dev,
                         double* scores_dev, int64_t* rows_dev, void* stream) {
   std::lock_guard<std::mutex> lk(r->mu);

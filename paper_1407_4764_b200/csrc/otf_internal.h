@@ -85,3 +85,10 @@ int launch_gather_i64(const int64_t* src, const int64_t* rows, int64_t n, int64_
                       int64_t* dst, cudaStream_t st);
 
 }  // namespace otf
+
+namespace otf {
+// many classifiers (otf_multi.cu): tcgen05 TF32x3 scoring, out (n_cls x n float32)
+bool multi_tc_supported(int d, const float* X);
+int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_cls, float* ws, float* out,
+                       int device, cudaStream_t st);
+}  // namespace otf

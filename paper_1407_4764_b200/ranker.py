@@ -304,6 +304,42 @@ class Repository:
         return Repository(self.kind, h, self._model_dim, self.ids[keep], names, codebook=self._codebook,
                           codec=self._codec, output_bits=self._output_bits)
 
+    # -- many classifiers at once (C5b; tensor cores, dense repositories) -------------------------
+    def _weight_matrix(self, models) -> np.ndarray:
+        rows = [as_weights(m) for m in models]
+        W = np.ascontiguousarray(np.stack(rows), dtype=np.float64)
+        if W.ndim != 2 or W.shape[1] != self._model_dim:
+            raise ConfigError(f"store dim {self._model_dim} does not match model dim {W.shape[-1]}")
+        return W
+
+    def score_many(self, models) -> np.ndarray:
+        """(len(models), count) float32 scores — one score_dense per model (ranker.py:63-69),
+        computed together on the tcgen05 tensor cores (TF32 with a 3-product split)."""
+        W = self._weight_matrix(models)
+        out = np.empty((W.shape[0], self.count), dtype=np.float32)
+        _lib.check(_lib.load().otf_repo_score_many(self._handle, _lib.ptr(W), W.shape[0], _lib.ptr(out),
+                                                   _lib.MEM_HOST, None))
+        return out
+
+    def rank_many(self, models, k: int, produced_at: float = 0.0) -> list[RankedList]:
+        """[self.rank(m, k) for m in models], scored together on the tensor cores."""
+        W = self._weight_matrix(models)
+        k_eff = max(0, min(int(k), self.count))
+        ids = np.empty((W.shape[0], k_eff), dtype=np.int64)
+        sc = np.empty((W.shape[0], k_eff), dtype=np.float64)
+        got = C.c_int64(0)
+        if k_eff:
+            _lib.check(_lib.load().otf_repo_rank_many(self._handle, _lib.ptr(W), W.shape[0], k_eff, _lib.ptr(ids),
+                                                      _lib.ptr(sc), C.byref(got), _lib.MEM_HOST, None))
+        out = []
+        row_of = None
+        if self.names is not None:
+            row_of = {int(v): i for i, v in enumerate(self.ids)}
+        for i, m in enumerate(models):
+            names = tuple(self.names[row_of[int(x)]] for x in ids[i]) if row_of is not None else None
+            out.append(RankedList(ids[i].copy(), sc[i].copy(), model_version(m), produced_at, names))
+        return out
+
     def rank(self, model, k: int, produced_at: float = 0.0) -> RankedList:
         w = self._weights(model)
         n = self.count

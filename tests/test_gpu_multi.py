@@ -1,0 +1,73 @@
+"""Many classifiers at once (C5b) on the tcgen05 tensor cores, through the C ABI.
+
+Bar: every classifier's scores stay within the reference tolerance of its own score_dense
+(ranker.py:63-69; 1e-6 * ||w|| * ||x||) and within the documented error of the TF32x3 split of
+the exact dot; rank_many equals the oracle's exact top_k of those scores; a row's scores do not
+depend on its position (128-row tiles, padding rows, permutations).
+"""
+
+import numpy as np
+import pytest
+
+import otf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def exact(x, W):
+    return x.astype(np.float64) @ W.astype(np.float32).astype(np.float64).T
+
+
+@pytest.mark.parametrize("n,d,c", [(1000, 128, 7), (129, 32, 1), (4096, 256, 64), (777, 4096, 3), (300, 2048, 70)])
+def test_score_many_matches_dense(otf, n, d, c):
+    rng = np.random.default_rng(n + d + c)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    W = rng.standard_normal((c, d))
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    S = repo.score_many(list(W))
+    assert S.shape == (c, n) and S.dtype == np.float32
+    ex = exact(x, W).T
+    mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
+    # TF32 x3: dropped lo*lo and TF32 rounding of the lo parts (~2^-20 relative per product)
+    # plus float32 accumulation in the tensor core
+    assert np.all(np.abs(S - ex) <= 2.0 ** -18 * mag + np.spacing(np.abs(S)) + 1e-30)
+    for i in range(min(c, 5)):
+        ref = O.score_dense(W[i], x)
+        assert np.max(np.abs(S[i].astype(np.float64) - ref)) <= 1e-6 * np.linalg.norm(W[i]) * 1.0001
+
+
+def test_score_many_position_independent(otf):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((1500, 512)).astype(np.float32)
+    W = rng.standard_normal((16, 512))
+    S = otf.Repository.dense(otf.FeatureStore(x)).score_many(list(W))
+    perm = rng.permutation(1500)
+    S2 = otf.Repository.dense(otf.FeatureStore(x[perm])).score_many(list(W))
+    np.testing.assert_array_equal(S2, S[:, perm])
+
+
+def test_rank_many_exact_topk(otf):
+    rng = np.random.default_rng(9)
+    n, d, c, k = 20_000, 256, 12, 300
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    ids = rng.permutation(3 * n)[:n].astype(np.int64)
+    W = rng.standard_normal((c, d))
+    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    S = repo.score_many(list(W))
+    lists = repo.rank_many([otf.LinearModel(w, 1, 3) for w in W], k)
+    assert len(lists) == c
+    for i in range(c):
+        o_ids, o_sc, _ = O.top_k(S[i], k, ids)
+        np.testing.assert_array_equal(lists[i].ids, o_ids)
+        np.testing.assert_array_equal(lists[i].scores, o_sc)
+        assert lists[i].model_version == 3
+
+
+def test_multi_errors(otf):
+    repo = otf.Repository.dense(otf.FeatureStore(np.ones((10, 30), np.float32)))
+    with pytest.raises(otf.ConfigError):
+        repo.score_many([np.ones(30)])  # dim % 32 != 0
+    repo2 = otf.Repository.dense(otf.FeatureStore(np.ones((10, 64), np.float32)))
+    with pytest.raises(otf.ConfigError):
+        repo2.score_many([np.ones(32)])
