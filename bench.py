@@ -48,6 +48,9 @@ CONFIGS = {
                workload="C3: 10M PQ codes per GPU (16 sub-quantizers x 256 centroids, 128-D), LUT score + top-1000"),
     "c5a": dict(kind="binary", rows=100_000_000, dim=2048, k=1000,
                 workload="C5a: 100M x 2048-bit packed binary codes per GPU, score + top-1000"),
+    "c5b": dict(kind="multi", rows=10_000_000, dim=4096, k=1000, n_cls=64,
+                workload="C5b: 64 concurrent classifiers over 10M x 4096-D fp32 rows per GPU "
+                         "(tcgen05 TF32x3 skinny GEMM) + exact top-1000 per classifier"),
 }
 
 
@@ -60,7 +63,7 @@ def load_peaks():
 
 
 def row_bytes(cfg) -> int:
-    if cfg["kind"] == "dense":
+    if cfg["kind"] in ("dense", "multi"):
         return 4 * cfg["dim"]
     if cfg["kind"] == "pq":
         return cfg["dim"]
@@ -128,10 +131,16 @@ def cpu_sample(cfg, seed=1234):
 
     rng = np.random.default_rng(seed)
     kind, dim, k = cfg["kind"], cfg["dim"], cfg["k"]
-    if kind == "dense":
+    if kind in ("dense", "multi"):
         rows = max(20_000, min(cfg["rows"], (1 << 30) // (4 * dim)))  # <= 1 GiB of features
         x = rng.standard_normal((rows, dim), dtype=np.float32)
         x /= np.linalg.norm(x, axis=1, keepdims=True)
+        if kind == "multi":  # the reference API has one score_dense + top_k per classifier
+            W = rng.standard_normal((cfg["n_cls"], dim))
+            fn = lambda: [O.top_k(O.score_dense(w, x), k) for w in W]
+            desc = (f"{cfg['n_cls']} classifiers x {rows} x {dim}-D fp32 rows (one score_dense + top_k per "
+                    "classifier, ranker.py:63-143); unit = image-classifier pairs")
+            return rows * cfg["n_cls"], fn, desc
         w = rng.standard_normal(dim)
         fn = lambda: O.top_k(O.score_dense(w, x), k)
         desc = f"{rows} x {dim}-D fp32 rows (score_dense + top_k, ranker.py:63-143)"
@@ -208,7 +217,7 @@ def make_repository(cfg, rank, world, device, seed=20260418):
     g = torch.Generator(device=dev)
     g.manual_seed(seed + 7919 * rank)
     keep = {}
-    if cfg["kind"] == "dense":
+    if cfg["kind"] in ("dense", "multi"):
         d = cfg["dim"]
         x = torch.empty((n, d), dtype=torch.float32, device=dev)
         chunk = max(1, (1 << 28) // d)
@@ -264,8 +273,23 @@ def run_gpu(args, cfg):
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
     lib = _lib.load()
+    multi = cfg["kind"] == "multi"
+    n_cls = cfg.get("n_cls", 1)  # results per image (classifiers scored together)
+    if multi:
+        Wm = np.random.default_rng(99).standard_normal((n_cls, dim))
+        W_dev = torch.as_tensor(Wm, device=dev)
+        m_ids = torch.empty((n_cls, k), dtype=torch.int64, device=dev)
+        m_sc = torch.empty((n_cls, k), dtype=torch.float64, device=dev)
+        m_got = C.c_int64()
 
-    if world > 1:
+    if multi:
+        if world > 1:
+            raise SystemExit("c5b runs one replica per GPU; use --gpus 1")
+
+        def step():
+            _lib.check(lib.otf_repo_rank_many(repo.handle, _lib.tptr(W_dev), n_cls, k, _lib.tptr(m_ids),
+                                              _lib.tptr(m_sc), C.byref(m_got), _lib.MEM_DEVICE, sp))
+    elif world > 1:
         sharded = ShardedRepository.from_local(repo, total_rows, start)
         step = lambda: sharded.rank_device(w_dev, k)
     else:
@@ -315,10 +339,11 @@ def run_gpu(args, cfg):
         lt = torch.tensor([launches], device=dev, dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt.item())
-    value = total_rows / (ms / 1e3)
+    value = total_rows * n_cls / (ms / 1e3)
 
     # ---- dominant kernel (scoring) alone, event-timed: roofline ---------------------------
-    score_buf = torch.empty(n_local, dtype=torch.float64 if cfg["kind"] == "pq" else torch.float32, device=dev)
+    score_buf = torch.empty(n_local * n_cls, dtype=torch.float64 if cfg["kind"] == "pq" else torch.float32,
+                            device=dev)
     reps = max(5, min(50, args.steps))
     ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kms = []
@@ -326,7 +351,11 @@ def run_gpu(args, cfg):
         if flush:
             scratch.add_(1.0)
         ks.record(stream)
-        _lib.check(lib.otf_repo_score(repo.handle, _lib.tptr(w_dev), _lib.tptr(score_buf), _lib.MEM_DEVICE, sp))
+        if multi:
+            _lib.check(lib.otf_repo_score_many(repo.handle, _lib.tptr(W_dev), n_cls, _lib.tptr(score_buf),
+                                               _lib.MEM_DEVICE, sp))
+        else:
+            _lib.check(lib.otf_repo_score(repo.handle, _lib.tptr(w_dev), _lib.tptr(score_buf), _lib.MEM_DEVICE, sp))
         ke.record(stream)
         torch.cuda.synchronize(dev)
         kms.append(ks.elapsed_time(ke))
@@ -344,7 +373,10 @@ def run_gpu(args, cfg):
     # ---- end to end through the public API (host w in, host RankedList out) ---------------
     e2e_steps = max(3, min(args.steps, 200))
     model = otf.LinearModel(w, 1, 1)
-    if world > 1:
+    if multi:
+        models = [otf.LinearModel(wc, 1, 1) for wc in Wm]
+        api = lambda: repo.rank_many(models, k)
+    elif world > 1:
         api = lambda: sharded.rank(model, k, root_only=True)
     else:
         api = lambda: repo.rank(model, k)
@@ -366,7 +398,8 @@ def run_gpu(args, cfg):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_val = total_rows / e2e_s
+    e2e_val = total_rows * n_cls / e2e_s
+    unit = "image-classifier pairs/s" if multi else "images/s"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -377,14 +410,14 @@ def run_gpu(args, cfg):
             t0 = time.perf_counter()
             fn()
             tt.append(time.perf_counter() - t0)
-        cpu = {"value": rows / min(tt), "unit": "images/s", "cores": cpu_threads(), "kind": "port",
+        cpu = {"value": rows / min(tt), "unit": unit, "cores": cpu_threads(), "kind": "port",
                "sample": desc + ", oracle port (numpy) best of 3 on this host"}
 
     if rank == 0:
         line = {
             "metric": "dataset images scored+ranked/sec",
             "value": value,
-            "unit": "images/s",
+            "unit": unit,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
@@ -392,7 +425,8 @@ def run_gpu(args, cfg):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": (value / cfg["published"]) if cfg.get("published") else None,
-            "dtype": {"dense": "f32 (f64 accumulate)", "pq": "f64", "binary": "f32 (f64 accumulate)"}[cfg["kind"]],
+            "dtype": {"dense": "f32 (f64 accumulate)", "pq": "f64", "binary": "f32 (f64 accumulate)",
+                      "multi": "f32 via tcgen05 tf32x3"}[cfg["kind"]],
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "rows_per_gpu": n_local, "total_rows": total_rows,
                        "dim_or_blocks_or_bits": cfg["dim"], "k": k, "parallelism": f"dp{world} (rows sharded)",
@@ -400,11 +434,13 @@ def run_gpu(args, cfg):
                               f"inputs ({payload / 1e9:.1f} GB/GPU) larger than L2")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"{cfg['kind']} score (otf_repo_score: scan of {payload / 1e9:.3f} GB)",
+                         "kernel": (f"multi_score_tc (tcgen05 tf32x3, {n_cls} classifiers) over {payload / 1e9:.3f} GB"
+                                    if multi else
+                                    f"{cfg['kind']} score (otf_repo_score: scan of {payload / 1e9:.3f} GB)"),
                          "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms, "peak_source": peak_src},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": dim * 8,
-                    "d2h_bytes_per_step": k * 24, "ms_per_query": e2e_s * 1e3},
+            "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": dim * 8 * n_cls,
+                    "d2h_bytes_per_step": k * (16 if multi else 24) * n_cls, "ms_per_query": e2e_s * 1e3},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

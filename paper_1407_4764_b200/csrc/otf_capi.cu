@@ -114,7 +114,7 @@ struct otf_repo {
   float* cents = nullptr;          // pq centroids (device)
   cudaStream_t stream = nullptr;
   std::mutex mu;                   // one call at a time per handle
-  DevBuf w, w32, lut, scores, bins, outbuf;
+  DevBuf w, w32, lut, scores, bins, outbuf, multi;  // multi: (<=64, n) float32 classifier scores
   HostBuf h_w, h_out;
   TopkWs topk;
   // graph cache for otf_repo_rank_graph
@@ -203,6 +203,7 @@ void repo_free(otf_repo* r) {
   if (r->ids) cudaFree(r->ids);
   if (r->cents) cudaFree(r->cents);
   r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->bins.release(); r->outbuf.release();
+  r->multi.release();
   r->h_w.release(); r->h_out.release();
   topk_ws_free(&r->topk);
   if (r->stream) cudaStreamDestroy(r->stream);
@@ -535,7 +536,7 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   if (k_eff == 0) return OTF_OK;
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
   const size_t wbytes = (size_t)n_cls * r->model_dim * sizeof(double);
-  DevBuf dW, dIds, dSc, scores;
+  DevBuf dW, dIds, dSc;
   const double* wp = W;
   int rc = OTF_OK;
   if (mem == OTF_MEM_HOST) {
@@ -546,22 +547,23 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   }
   int64_t* ids = mem == OTF_MEM_HOST ? static_cast<int64_t*>(dIds.p) : out_ids;
   double* sc = mem == OTF_MEM_HOST ? static_cast<double*>(dSc.p) : out_scores;
-  if ((rc = scores.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
+  // the (<= 64, n) score buffer is cached on the handle (2.56 GB for 64 x 10M rows)
+  if ((rc = r->multi.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
+  float* sbuf = static_cast<float*>(r->multi.p);
   for (int c0 = 0; c0 < n_cls && !rc; c0 += 64) {
     const int cn = std::min(64, n_cls - c0);
-    rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, static_cast<float*>(scores.p), st);
+    rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, sbuf, st);
     for (int c = 0; c < cn && !rc; ++c)
-      rc = launch_topk(static_cast<const float*>(scores.p) + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base,
-                       k_eff, &r->topk, false, ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff,
-                       nullptr, r->device, st);
+      rc = launch_topk(sbuf + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base, k_eff, &r->topk, false,
+                       ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff, nullptr, r->device, st);
   }
   if (!rc && mem == OTF_MEM_HOST) {
     cudaError_t e = cudaMemcpyAsync(out_ids, ids, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_scores, sc, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
   }
-  cudaStreamSynchronize(st);  // the score buffer is released on return
-  dW.release(); dIds.release(); dSc.release(); scores.release();
+  if (mem == OTF_MEM_HOST || rc) cudaStreamSynchronize(st);
+  dW.release(); dIds.release(); dSc.release();
   return rc;
 }
 
