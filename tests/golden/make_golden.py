@@ -154,6 +154,27 @@ def main() -> None:
         g[f"tb_{name}_hist"] = np.array(hist)
         g[f"tb_{name}_obj"] = np.array([rt.hinge_objective(model.weights, feats, labels, 1.0 / (0.25 * len(feats)))])
 
+    # ---- live session replay (session.py:237-290) ---------------------------------------------
+    from otf_retrieval import session as rs
+    from otf_retrieval.store import SynthConfig, generate_corpus_bundle
+
+    bundle = generate_corpus_bundle(SynthConfig(dim=32, classes=3, per_class=40, distractors=3000, seed=51),
+                                    train_per_class=30, negative_count=400)
+    repo = rr.Repository.dense(bundle.test)
+    cfg = rs.SessionConfig(rate=12.0, ranker=rr.RankerConfig(k=25, interval=0.18),
+                           trainer=rt.TrainerConfig(lam=0.1, batch_size=16), steps_per_second=100.0)
+    sess = rs.QuerySession("s", "class_00", repo, bundle.negatives.data, cfg, trainer_seed=5)
+    train_rows = sorted(bundle.train_labels.ids_for("class_00"))
+    feed = bundle.train.data[train_rows]
+    pubs = []
+    rs.run_simulated(sess, feed, 2.0, on_publish=pubs.append)
+    g["sess_test_x"], g["sess_neg"], g["sess_feed"] = bundle.test.data, bundle.negatives.data, feed
+    g["sess_ids"] = np.stack([p.ranked.ids for p in pubs])
+    g["sess_meta"] = np.array([[p.ranked.model_version, p.positives_fed, p.steps_applied, p.lists_published]
+                               for p in pubs])
+    g["sess_at"] = np.array([p.ranked.produced_at for p in pubs])
+    g["sess_w"] = sess.trainer.snapshot().weights
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
 
