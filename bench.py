@@ -460,7 +460,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if os.environ.get("OTF_BENCH_ROWS"):  # profiling runs only: shrink the repository
+        cfg["rows"] = int(os.environ["OTF_BENCH_ROWS"])
     if args.steps is None:
         args.steps = 20 if args.impl == "reference" else 500
     args.warmup = max(args.warmup, 3)

@@ -4,23 +4,30 @@
 // ranks the same repository under 64 classifiers, i.e. a skinny GEMM (N = 64) with 32 flop/B —
 // float32 SIMT (~70 TFLOP/s) would be 3x slower than HBM, so it runs on tcgen05 in TF32 with a
 // 3-product split for float32-level accuracy:
-//     x·w ≈ x_hi·w_hi + x_hi·w_lo + x_lo·w_hi,   v_hi = tf32(v) (the MMA reads the top 19 bits),
-//                                                 v_lo = v − v_hi (exact in float32).
+//     x·w ≈ x_hi·w_hi + x_hi·w_lo + x_lo·w_hi,   v_hi = v with the low 13 mantissa bits cleared
+//                                                 (exact TF32), v_lo = v − v_hi (exact float32).
 // W (≤ 64 classifiers) is split once on the device into a stacked [w_hi; w_lo] (128 × d) matrix,
 // so one N=128 MMA computes x_hi·w_hi (accumulator columns 0..63) and x_hi·w_lo (64..127), and a
 // second N=64 MMA adds x_lo·w_hi into columns 64..127; the epilogue adds the two halves.
 //
 // Per CTA (one per SM, persistent over 128-row tiles), warp-specialised:
 //   warp 0      TMA producer: X tile (128 rows × 32 floats, SWIZZLE_128B) + W tile per stage
-//   warp 1      MMA issuer (one elected thread): 4 K-steps × (N=128 + N=64) tcgen05.mma per stage
-//   warp 2      TMEM allocator (2 × 128 accumulator columns, double-buffered across tiles)
+//               (6-stage shared-memory ring, 32 KB per stage)
+//   warp 1      MMA issuer (one thread): per stage 4 K-steps × (N=128 + N=64) tcgen05.mma with the
+//               A operands read from TMEM (kind::tf32, A in TMEM, B = W from shared memory)
+//   warp 2      TMEM allocator (512 columns: 2 × 128 accumulators + 4 × 64 A slots)
 //   warps 4–7   epilogue: tcgen05.ld the accumulators, sum halves, store scores (classifier-major)
-//   warps 8–11  split: x_lo = x − tf32(x) for each stage into a second shared-memory tile
+//   warps 8–11  split: thread r reads row r of the swizzled X tile, writes x_hi and x_lo of that row
+//               into a TMEM A slot (tcgen05.st) and frees the shared-memory X tile right away
+// Keeping the split operands in TMEM halves the shared-memory traffic per stage (no x_lo tile, no
+// A reads from shared memory) and lets the ring hold 6 stages of X in flight.
 // Every output row is computed by the same MMA sequence whatever its tile, so a row's scores do
 // not depend on its position. Parity is a tolerance against the reference's float32 sgemv
 // (DESIGN.md §Parity); ranking of each classifier is the exact top-k of these scores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "otf_common.cuh"
 #include "otf_internal.h"
@@ -29,12 +36,14 @@ namespace otf {
 
 constexpr int kMT = 128;          // rows per tile (UMMA M)
 constexpr int kKC = 32;           // K floats per stage (128 bytes = one swizzle row)
-constexpr int kStages = 4;
+constexpr int kStages = 6;        // shared-memory ring: X tile + W tile per stage
+constexpr int kASlots = 4;        // TMEM ring for the split A operands (x_hi | x_lo)
 constexpr int kTileX = kMT * kKC * 4;   // 16 KB
 constexpr int kTileW = 128 * kKC * 4;   // 16 KB (stacked w_hi; w_lo)
-constexpr int kStageBytes = 2 * kTileX + kTileW;
-constexpr int kMultiThreads = 384;
-constexpr int kTmemCols = 256;
+constexpr int kStageBytes = kTileX + kTileW;
+constexpr int kMultiThreads = 512;  // 16 warps: producer, MMA, alloc, -, 4 epilogue, 8 split
+constexpr int kTmemCols = 512;    // 2 x 128 accumulator columns + 4 x 64 A columns
+constexpr int kAccCols = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -90,28 +99,49 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
          | ((uint32_t)(n >> 3) << 17)  // N >> 3
          | ((uint32_t)(kMT >> 4) << 24);  // M >> 4
 }
-__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
+// D[tmem] (+)= A[tmem] · B[smem]ᵀ
+__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 
 __global__ void __launch_bounds__(kMultiThreads, 1)
 multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
-               int64_t n, int d, int n_cls, float* __restrict__ out) {
+               int64_t n, int d, int n_cls, float* __restrict__ out, int mode) {
+  // mode: 0 in production; diagnostic bits (OTF_MULTI_MODE) switch parts off to find the
+  // bottleneck: 1 = no MMA, 2 = no TMEM stores in the split, 4 = no score stores.
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full_tma[kStages], full_split[kStages], empty[kStages];
+  __shared__ uint64_t full[kStages], empty[kStages];   // smem ring (empty: 4 split warps + MMA)
+  __shared__ uint64_t a_full[kASlots], a_empty[kASlots];  // TMEM A ring
   __shared__ uint64_t tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base_slot;
 
@@ -121,9 +151,12 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_tma[s], 1);
-      mbar_init(&full_split[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 5);
+    }
+    for (int a = 0; a < kASlots; ++a) {
+      mbar_init(&a_full[a], 4);
+      mbar_init(&a_empty[a], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
@@ -147,16 +180,30 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      // L2 prefetch runs kPrefetch chunks ahead of the shared-memory ring, so ~2x the ring's
+      // bytes are in flight from HBM (the ring alone left the SM latency-bound)
+      constexpr int kPrefetch = 8;
+      int64_t pf_tile = blockIdx.x;
+      int pf_kc = 0;
+      auto prefetch_next = [&]() {
+        if (pf_tile >= n_tiles) return;
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map_x),
+                     "r"(pf_kc * kKC), "r"((int)(pf_tile * kMT))
+                     : "memory");
+        if (++pf_kc == kchunks) { pf_kc = 0; pf_tile += gridDim.x; }
+      };
+      for (int p = 0; p < kPrefetch; ++p) prefetch_next();
       uint32_t it = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int kc = 0; kc < kchunks; ++kc, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
+          prefetch_next();
           mbar_wait(&empty[s], ph ^ 1u);
           unsigned char* st = smem + s * kStageBytes;
-          mbar_expect_tx(&full_tma[s], kTileX + kTileW);
-          tma_load_2d(st, &map_x, &full_tma[s], kc * kKC, (int)(tile * kMT));
-          tma_load_2d(st + 2 * kTileX, &map_w, &full_tma[s], kc * kKC, 0);
+          mbar_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(st, &map_x, &full[s], kc * kKC, (int)(tile * kMT));
+          tma_load_2d(st + kTileX, &map_w, &full[s], kc * kKC, 0);
         }
       }
     }
@@ -173,20 +220,23 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
         for (int kc = 0; kc < kchunks; ++kc, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
-          mbar_wait(&full_tma[s], ph);
-          mbar_wait(&full_split[s], ph);
+          const int a = it % kASlots;
+          const uint32_t aph = (it / kASlots) & 1u;
+          mbar_wait(&full[s], ph);     // W tile landed
+          mbar_wait(&a_full[a], aph);  // x_hi / x_lo written to TMEM
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t xa = smem_u32(smem + s * kStageBytes);
-          const uint32_t xl = xa + kTileX;
-          const uint32_t wa = xa + 2 * kTileX;
+          const uint32_t wa = smem_u32(smem + s * kStageBytes + kTileX);
+          const uint32_t ahi = tmem_base + kAccCols + a * 64;
+          if (!(mode & 1)) {
 #pragma unroll
-          for (int k = 0; k < kKC / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
-            const uint32_t off = k * 32;
-            umma_tf32(acc, umma_desc_sw128(xa + off), umma_desc_sw128(wa + off), id128,
-                      (kc | k) != 0);
-            umma_tf32(acc + 64, umma_desc_sw128(xl + off), umma_desc_sw128(wa + off), id64, 1u);
+            for (int k = 0; k < kKC / 8; ++k) {  // K = 8 tf32 per MMA: 8 TMEM columns / 32 B of W
+              umma_tf32_ts(acc, ahi + k * 8, umma_desc_sw128(wa + k * 32), (mode & 8) ? id64 : id128,
+                           (kc | k) != 0);
+              if (!(mode & 16)) umma_tf32_ts(acc + 64, ahi + 32 + k * 8, umma_desc_sw128(wa + k * 32), id64, 1u);
+            }
           }
-          umma_commit(&empty[s]);
+          umma_commit(&empty[s]);    // W tile consumed
+          umma_commit(&a_empty[a]);  // A slot consumed
         }
         umma_commit(&tmem_full[b]);
       }
@@ -204,24 +254,15 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 16) {
         uint32_t h[16], l[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(h[0]), "=r"(h[1]), "=r"(h[2]), "=r"(h[3]), "=r"(h[4]), "=r"(h[5]), "=r"(h[6]),
-              "=r"(h[7]), "=r"(h[8]), "=r"(h[9]), "=r"(h[10]), "=r"(h[11]), "=r"(h[12]), "=r"(h[13]),
-              "=r"(h[14]), "=r"(h[15])
-            : "r"(taddr + c0));
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(l[0]), "=r"(l[1]), "=r"(l[2]), "=r"(l[3]), "=r"(l[4]), "=r"(l[5]), "=r"(l[6]),
-              "=r"(l[7]), "=r"(l[8]), "=r"(l[9]), "=r"(l[10]), "=r"(l[11]), "=r"(l[12]), "=r"(l[13]),
-              "=r"(l[14]), "=r"(l[15])
-            : "r"(taddr + 64 + c0));
+        tmem_ld16(taddr + c0, h);
+        tmem_ld16(taddr + 64 + c0, l);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < n) {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             const int c = c0 + t;
-            if (c < n_cls) out[(int64_t)c * n + row] = __fadd_rn(__uint_as_float(h[t]), __uint_as_float(l[t]));
+            if (c < n_cls && !(mode & 4))
+              out[(int64_t)c * n + row] = __fadd_rn(__uint_as_float(h[t]), __uint_as_float(l[t]));
           }
         }
       }
@@ -230,36 +271,49 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
       if (lane == 0) mbar_arrive(&tmem_empty[b]);
     }
   } else if (warp >= 8) {
-    // ---------------- split: x_lo = x - tf32(x) ----------------
-    const int t = threadIdx.x - 256;  // 0..127
+    // ---------------- split: row r -> x_hi, x_lo in TMEM ----------------
+    // two warpgroups alternate chunks (even / odd) so one chunk's TMEM store latency overlaps
+    // the next chunk's shared-memory reads
+    const int q = warp & 3;             // TMEM lane quadrant of this warp
+    const uint32_t par = (uint32_t)((warp - 8) >> 2);
+    const int r = 32 * q + lane;        // tile row handled by this thread
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     uint32_t it = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        if ((it & 1u) != par) continue;
         const int s = it % kStages;
         const uint32_t ph = (it / kStages) & 1u;
-        mbar_wait(&full_tma[s], ph);
-        // x_hi = x with the low 13 mantissa bits cleared (written back in place, so the tensor
-        // core sees an exact TF32 value whether it truncates or rounds), x_lo = x - x_hi (exact).
-        float4* hi = reinterpret_cast<float4*>(smem + s * kStageBytes);
-        float4* dst = reinterpret_cast<float4*>(smem + s * kStageBytes + kTileX);
+        const int a = it % kASlots;
+        const uint32_t aph = (it / kASlots) & 1u;
+        mbar_wait(&full[s], ph);
+        // row r of the SWIZZLE_128B tile: 16-byte chunk c sits at chunk position c ^ (r & 7)
+        const unsigned char* rowp = smem + s * kStageBytes + r * 128;
+        uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int i = 0; i < kTileX / 16 / 128; ++i) {  // 8 float4 per thread
-          const float4 v = hi[t + 128 * i];
-          float4 h, lo;
-          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          lo.x = __fsub_rn(v.x, h.x);
-          lo.y = __fsub_rn(v.y, h.y);
-          lo.z = __fsub_rn(v.z, h.z);
-          lo.w = __fsub_rn(v.w, h.w);
-          hi[t + 128 * i] = h;
-          dst[t + 128 * i] = lo;
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t h = __float_as_uint(e[t]) & 0xFFFFE000u;
+            hi[4 * c + t] = h;
+            lo[4 * c + t] = __float_as_uint(__fsub_rn(e[t], __uint_as_float(h)));
+          }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full_split[s]);
+        if (lane == 0) mbar_arrive(&empty[s]);  // X tile read: the producer may refill it
+        mbar_wait(&a_empty[a], aph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t aaddr = tmem_base + lane_off + kAccCols + a * 64;
+        if (!(mode & 2)) {
+          tmem_st32(aaddr, hi);
+          tmem_st32(aaddr + 32, lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[a]);
       }
     }
   }
@@ -336,7 +390,8 @@ int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_
   const int64_t tiles = (n + kMT - 1) / kMT;
   int grid = sm_count(device);
   if (tiles < grid) grid = (int)tiles;
-  multi_score_tc<<<grid, kMultiThreads, smem, st>>>(mx, mw, n, d, n_cls, out);
+  static const int mode = getenv("OTF_MULTI_MODE") ? atoi(getenv("OTF_MULTI_MODE")) : 0;
+  multi_score_tc<<<grid, kMultiThreads, smem, st>>>(mx, mw, n, d, n_cls, out, mode);
   OTF_LAUNCH_CHECK("multi_score_tc");
   return OTF_OK;
 }
