@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     procs = []
     for src in SOURCES:
         obj = OBJ / (Path(src).stem + ".o")
-        cmd = [cc, *FLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
+        extra = os.environ.get("OTF_NVCC_EXTRA", "").split()  # diagnostic variants (tools/)
+        cmd = [cc, *FLAGS, *extra, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
         if ptxas_verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         if verbose:

@@ -36,14 +36,35 @@ namespace otf {
 
 constexpr int kMT = 128;          // rows per tile (UMMA M)
 constexpr int kKC = 32;           // K floats per stage (128 bytes = one swizzle row)
-constexpr int kStages = 6;        // shared-memory ring: X tile + W tile per stage
-constexpr int kASlots = 4;        // TMEM ring for the split A operands (x_hi | x_lo)
+#ifndef OTF_MULTI_XSTAGES
+#define OTF_MULTI_XSTAGES 8
+#endif
+#ifndef OTF_MULTI_WSTAGES
+#define OTF_MULTI_WSTAGES 4
+#endif
+constexpr int kXStages = OTF_MULTI_XSTAGES;  // shared-memory ring of X tiles (freed by the split warps)
+constexpr int kWStages = OTF_MULTI_WSTAGES;  // shared-memory ring of W tiles (freed by the MMAs)
+#ifndef OTF_MULTI_ACC_BUFS
+#define OTF_MULTI_ACC_BUFS 2
+#endif
+constexpr int kAccBufs = OTF_MULTI_ACC_BUFS;  // accumulators (128 TMEM columns each)
+#ifndef OTF_MULTI_TSHI
+#define OTF_MULTI_SSHI 1
+#endif
+#ifdef OTF_MULTI_SSHI
+// x_hi is not materialised: the N=128 MMA reads the raw X tile from shared memory (the tensor
+// core reads float32 operands of kind::tf32 as their TF32 truncation) and only x_lo goes to TMEM
+constexpr int kASlotCols = 32;
+#else
+constexpr int kASlotCols = 64;
+#endif
+constexpr int kASlots = (512 - 128 * kAccBufs) / kASlotCols;  // TMEM ring for the split A operands
 constexpr int kTileX = kMT * kKC * 4;   // 16 KB
 constexpr int kTileW = 128 * kKC * 4;   // 16 KB (stacked w_hi; w_lo)
-constexpr int kStageBytes = kTileX + kTileW;
+constexpr int kRingBytes = kXStages * kTileX + kWStages * kTileW;
 constexpr int kMultiThreads = 512;  // 16 warps: producer, MMA, alloc, -, 4 epilogue, 8 split
 constexpr int kTmemCols = 512;    // 2 x 128 accumulator columns + 4 x 64 A columns
-constexpr int kAccCols = 256;
+constexpr int kAccCols = 128 * kAccBufs;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -79,6 +100,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
           "r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// expect_tx(bytes) + 2D TMA load of one box, issued by one elected lane of a converged warp
+__device__ __forceinline__ void tma_load_elect(void* dst, const CUtensorMap* map, uint64_t* bar, uint32_t bytes,
+                                               int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%4, %5}], [%2];\n\t}" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(bytes), "r"(c0), "r"(c1)
       : "memory");
 }
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (rows of 128 B, 8-row atoms of 1 KB).
@@ -140,9 +172,10 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   // 1024-byte alignment for the swizzled tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[kStages], empty[kStages];   // smem ring (empty: 4 split warps + MMA)
+  __shared__ uint64_t full[kXStages], empty[kXStages];     // X ring (empty: the 4 split warps)
+  __shared__ uint64_t wfull[kWStages], wempty[kWStages];   // W ring (empty: MMA commit)
   __shared__ uint64_t a_full[kASlots], a_empty[kASlots];  // TMEM A ring
-  __shared__ uint64_t tmem_full[2], tmem_empty[2];
+  __shared__ uint64_t tmem_full[kAccBufs], tmem_empty[kAccBufs];
   __shared__ uint32_t tmem_base_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,15 +183,23 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   const int kchunks = d / kKC;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kXStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 5);
+#ifdef OTF_MULTI_SSHI
+      mbar_init(&empty[s], 5);  // 4 split warps + the MMA commit
+#else
+      mbar_init(&empty[s], 4);
+#endif
+    }
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
     }
     for (int a = 0; a < kASlots; ++a) {
       mbar_init(&a_full[a], 4);
       mbar_init(&a_empty[a], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 4);
     }
@@ -177,77 +218,179 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = tmem_base_slot;
 
+  unsigned char* const xring = smem;
+  unsigned char* const wring = smem + kXStages * kTileX;
+  // Producers, like the MMA issuer, run their loops on the whole warp (warp-uniform operands in
+  // uniform registers) and issue from one elected lane inside the asm block.
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      // L2 prefetch runs kPrefetch chunks ahead of the shared-memory ring, so ~2x the ring's
-      // bytes are in flight from HBM (the ring alone left the SM latency-bound)
-      constexpr int kPrefetch = 8;
-      int64_t pf_tile = blockIdx.x;
-      int pf_kc = 0;
-      auto prefetch_next = [&]() {
-        if (pf_tile >= n_tiles) return;
-        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map_x),
-                     "r"(pf_kc * kKC), "r"((int)(pf_tile * kMT))
-                     : "memory");
-        if (++pf_kc == kchunks) { pf_kc = 0; pf_tile += gridDim.x; }
-      };
+    // ---------------- TMA producer: X ----------------
+    // X tiles never wait on the tensor cores: the split warps free a stage as soon as they have
+    // read it, so the ring keeps kXStages x 16 KB of HBM reads in flight; the L2 prefetch runs
+    // kPrefetch chunks further ahead
+    constexpr int kPrefetch = 8;
+    int64_t pf_tile = blockIdx.x;
+    int pf_kc = 0;
+    auto prefetch_next = [&]() {
+      if (pf_tile >= n_tiles) return;
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n\t}" ::"l"(&map_x),
+          "r"(pf_kc * kKC), "r"((int)(pf_tile * kMT))
+          : "memory");
+      if (++pf_kc == kchunks) { pf_kc = 0; pf_tile += gridDim.x; }
+    };
+    if (!(mode & 32))
       for (int p = 0; p < kPrefetch; ++p) prefetch_next();
-      uint32_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for (int kc = 0; kc < kchunks; ++kc, ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1u;
-          prefetch_next();
-          mbar_wait(&empty[s], ph ^ 1u);
-          unsigned char* st = smem + s * kStageBytes;
-          mbar_expect_tx(&full[s], kStageBytes);
-          tma_load_2d(st, &map_x, &full[s], kc * kKC, (int)(tile * kMT));
-          tma_load_2d(st + kTileX, &map_w, &full[s], kc * kKC, 0);
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % kXStages;
+        const uint32_t ph = (it / kXStages) & 1u;
+        if (!(mode & 32)) prefetch_next();
+        mbar_wait(&empty[s], ph ^ 1u);
+#ifdef OTF_MULTI_LANE0
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], kTileX);
+          tma_load_2d(xring + s * kTileX, &map_x, &full[s], kc * kKC, (int)(tile * kMT));
         }
+#else
+        tma_load_elect(xring + s * kTileX, &map_x, &full[s], kTileX, kc * kKC, (int)(tile * kMT));
+#endif
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------- TMA producer: W (L2-resident, paced by the MMAs) ----------------
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % kWStages;
+        const uint32_t ph = (it / kWStages) & 1u;
+        mbar_wait(&wempty[s], ph ^ 1u);
+#ifdef OTF_MULTI_LANE0
+        if (lane == 0) {
+          mbar_expect_tx(&wfull[s], kTileW);
+          tma_load_2d(wring + s * kTileW, &map_w, &wfull[s], kc * kKC, 0);
+        }
+#else
+        if ((mode & 64) && it >= (uint32_t)kWStages) {  // diagnostic: no W traffic after the first ring
+          if (lane == 0) mbar_arrive(&wfull[s]);
+          continue;
+        }
+        tma_load_elect(wring + s * kTileW, &map_w, &wfull[s], kTileW, kc * kKC, 0);
+#endif
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      constexpr uint32_t id128 = idesc_tf32(128), id64 = idesc_tf32(64);
-      uint32_t it = 0, j = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
-        const int b = j & 1;
-        mbar_wait(&tmem_empty[b], ((j >> 1) & 1u) ^ 1u);
+    // The whole warp runs the loop (so every operand is warp-uniform and lives in uniform
+    // registers) and one elected lane issues a chunk's 8 MMAs + 2 commits in a single asm block:
+    // issued from a divergent single lane, each MMA became an ELECT/waterfall loop and the issue
+    // loop, not the tensor pipe, set the pace.
+    constexpr uint32_t id128 = idesc_tf32(128), id64 = idesc_tf32(64);
+    const uint64_t wdesc0 = umma_desc_sw128(smem_u32(wring));
+    const uint64_t xdesc0 = umma_desc_sw128(smem_u32(xring));
+    uint32_t it = 0, j = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+      const int b = j % kAccBufs;
+      mbar_wait(&tmem_empty[b], ((j / kAccBufs) & 1u) ^ 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t acc = tmem_base + b * 128;
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % kWStages;
+        const uint32_t ph = (it / kWStages) & 1u;
+        const int a = it % kASlots;
+        const uint32_t aph = (it / kASlots) & 1u;
+        mbar_wait(&wfull[s], ph);    // W tile landed
+        mbar_wait(&a_full[a], aph);  // x_hi / x_lo written to TMEM
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem_base + b * 128;
-        for (int kc = 0; kc < kchunks; ++kc, ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1u;
-          const int a = it % kASlots;
-          const uint32_t aph = (it / kASlots) & 1u;
-          mbar_wait(&full[s], ph);     // W tile landed
-          mbar_wait(&a_full[a], aph);  // x_hi / x_lo written to TMEM
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t wa = smem_u32(smem + s * kStageBytes + kTileX);
-          const uint32_t ahi = tmem_base + kAccCols + a * 64;
-          if (!(mode & 1)) {
-#pragma unroll
-            for (int k = 0; k < kKC / 8; ++k) {  // K = 8 tf32 per MMA: 8 TMEM columns / 32 B of W
-              umma_tf32_ts(acc, ahi + k * 8, umma_desc_sw128(wa + k * 32), (mode & 8) ? id64 : id128,
-                           (kc | k) != 0);
-              if (!(mode & 16)) umma_tf32_ts(acc + 64, ahi + 32 + k * 8, umma_desc_sw128(wa + k * 32), id64, 1u);
-            }
-          }
-          umma_commit(&empty[s]);    // W tile consumed
-          umma_commit(&a_empty[a]);  // A slot consumed
+        const uint64_t wd = wdesc0 + (uint64_t)((s * kTileW) >> 4);  // +32 B per K-step = +2
+#ifdef OTF_MULTI_SSHI
+        const int sx = it % kXStages;
+        mbar_wait(&full[sx], (it / kXStages) & 1u);
+        const uint64_t xd = xdesc0 + (uint64_t)((sx * kTileX) >> 4);
+        const uint32_t alo = tmem_base + kAccCols + a * kASlotCols;
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %6, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %7, p;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %9, %5, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%10], %5, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %11, %12, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%13], %12, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %14, %15, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%16], %15, %8, 1;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%17];\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%18];\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%19];\n\t}" ::"r"(acc),
+            "r"(acc + 64), "l"(xd), "r"(alo), "l"(wd), "l"(wd + 2), "r"(kc), "r"(id128), "r"(id64),
+            "l"(xd + 2), "r"(alo + 8), "l"(xd + 4), "l"(wd + 4), "r"(alo + 16), "l"(xd + 6), "l"(wd + 6),
+            "r"(alo + 24), "r"(smem_u32(&wempty[s])), "r"(smem_u32(&a_empty[a])), "r"(smem_u32(&empty[sx]))
+            : "memory");
+        continue;
+#endif
+        const uint32_t ahi = tmem_base + kAccCols + a * 64;
+        if (mode & 1) {
+          asm volatile(
+              "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t}" ::"r"(
+                  smem_u32(&wempty[s])),
+              "r"(smem_u32(&a_empty[a]))
+              : "memory");
+          continue;
         }
-        umma_commit(&tmem_full[b]);
+        if (mode & 24) {  // diagnostics: 4 MMAs per chunk, N = 128 (8) or N = 64 (16)
+          const uint32_t idx = (mode & 8) ? id128 : id64;
+          asm volatile(
+              "{\n\t.reg .pred e, p;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "setp.ne.b32 p, %3, 0;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%5], %6, %4, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%7], %8, %4, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %10, %4, 1;\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(acc),
+              "r"(ahi), "l"(wd), "r"(kc), "r"(idx), "r"(ahi + 8), "l"(wd + 2), "r"(ahi + 16), "l"(wd + 4),
+              "r"(ahi + 24), "l"(wd + 6), "r"(smem_u32(&wempty[s])), "r"(smem_u32(&a_empty[a]))
+              : "memory");
+          continue;
+        }
+        // K = 8 tf32 per MMA: 8 TMEM columns of A, 32 B (descriptor +2) of W per K-step
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %6, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %7, p;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %5, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%10], %5, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], %12, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%13], %12, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %15, %7, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%16], %15, %8, 1;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%17];\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%18];\n\t}" ::"r"(acc),
+            "r"(acc + 64), "r"(ahi), "r"(ahi + 32), "l"(wd), "l"(wd + 2), "r"(kc), "r"(id128), "r"(id64),
+            "r"(ahi + 8), "r"(ahi + 40), "r"(ahi + 16), "l"(wd + 4), "r"(ahi + 48), "r"(ahi + 24), "l"(wd + 6),
+            "r"(ahi + 56), "r"(smem_u32(&wempty[s])), "r"(smem_u32(&a_empty[a]))
+            : "memory");
       }
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+              smem_u32(&tmem_full[b]))
+          : "memory");
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
     uint32_t j = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
-      const int b = j & 1;
-      mbar_wait(&tmem_full[b], (j >> 1) & 1u);
+      const int b = j % kAccBufs;
+      mbar_wait(&tmem_full[b], (j / kAccBufs) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int64_t row = tile * kMT + 32 * q + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + b * 128;
@@ -282,13 +425,29 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kchunks; ++kc, ++it) {
         if ((it & 1u) != par) continue;
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1u;
+        const int s = it % kXStages;
+        const uint32_t ph = (it / kXStages) & 1u;
         const int a = it % kASlots;
         const uint32_t aph = (it / kASlots) & 1u;
         mbar_wait(&full[s], ph);
         // row r of the SWIZZLE_128B tile: 16-byte chunk c sits at chunk position c ^ (r & 7)
-        const unsigned char* rowp = smem + s * kStageBytes + r * 128;
+        const unsigned char* rowp = xring + s * kTileX + r * 128;
+#ifdef OTF_MULTI_SSHI
+        uint32_t lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            lo[4 * c + t] = __float_as_uint(__fsub_rn(e[t], __uint_as_float(__float_as_uint(e[t]) & 0xFFFFE000u)));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // X tile read (the MMA still reads it as x_hi)
+        mbar_wait(&a_empty[a], aph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (!(mode & 2)) tmem_st32(tmem_base + lane_off + kAccCols + a * kASlotCols, lo);
+#else
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -310,6 +469,7 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
           tmem_st32(aaddr, hi);
           tmem_st32(aaddr + 32, lo);
         }
+#endif
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
@@ -381,7 +541,7 @@ int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_
   int rc = make_map(&mx, X, (uint64_t)d, (uint64_t)n, kMT);
   if (!rc) rc = make_map(&mw, ws, (uint64_t)d, 128, 128);
   if (rc) return rc;
-  const size_t smem = (size_t)kStages * kStageBytes + 1024;
+  const size_t smem = (size_t)kRingBytes + 1024;
   static bool configured[64] = {false};
   if (!configured[device & 63]) {
     OTF_CUDA(cudaFuncSetAttribute((const void*)multi_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
