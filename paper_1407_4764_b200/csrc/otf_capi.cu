@@ -483,7 +483,7 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
 namespace {
 // scores for classifiers [c0, c0 + cn) into out (cn x n float32, classifier-major); W host/device.
 int multi_score_group(otf_repo* r, const double* dW, int cn, float* out, cudaStream_t st) {
-  int rc = r->w32.ensure((size_t)2 * 64 * r->model_dim * sizeof(float));
+  int rc = r->w32.ensure((size_t)multi_ws_floats(r->model_dim) * sizeof(float));
   if (rc) return rc;
   return launch_multi_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dW, cn,
                             static_cast<float*>(r->w32.p), out, r->device, st);

@@ -89,6 +89,8 @@ int launch_gather_i64(const int64_t* src, const int64_t* rows, int64_t n, int64_
 namespace otf {
 // many classifiers (otf_multi.cu): tcgen05 TF32x3 scoring, out (n_cls x n float32)
 bool multi_tc_supported(int d, const float* X);
+// float32 scratch launch_multi_score needs for the split, pre-tiled classifier matrix
+inline size_t multi_ws_floats(int d) { return (size_t)3 * 64 * (size_t)d; }
 int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_cls, float* ws, float* out,
                        int device, cudaStream_t st);
 }  // namespace otf

@@ -269,14 +269,14 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
 #ifdef OTF_MULTI_LANE0
         if (lane == 0) {
           mbar_expect_tx(&wfull[s], kTileW);
-          tma_load_2d(wring + s * kTileW, &map_w, &wfull[s], kc * kKC, 0);
+          tma_load_2d(wring + s * kTileW, &map_w, &wfull[s], 0, kc * 128);
         }
 #else
         if ((mode & 64) && it >= (uint32_t)kWStages) {  // diagnostic: no W traffic after the first ring
           if (lane == 0) mbar_arrive(&wfull[s]);
           continue;
         }
-        tma_load_elect(wring + s * kTileW, &map_w, &wfull[s], kTileW, kc * kKC, 0);
+        tma_load_elect(wring + s * kTileW, &map_w, &wfull[s], kTileW, 0, kc * 128);
 #endif
       }
     }
@@ -309,21 +309,32 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
         mbar_wait(&full[sx], (it / kXStages) & 1u);
         const uint64_t xd = xdesc0 + (uint64_t)((sx * kTileX) >> 4);
         const uint32_t alo = tmem_base + kAccCols + a * kASlotCols;
+        if (mode & 1) {
+          asm volatile(
+              "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%2];\n\t}" ::"r"(
+                  smem_u32(&wempty[s])),
+              "r"(smem_u32(&a_empty[a])), "r"(smem_u32(&empty[sx]))
+              : "memory");
+          continue;
+        }
         asm volatile(
             "{\n\t.reg .pred e, p;\n\t"
             "elect.sync _|e, 0xffffffff;\n\t"
             "setp.ne.b32 p, %6, 0;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %7, p;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %8, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %9, %5, %7, 1;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%10], %5, %8, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %11, %12, %7, 1;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%13], %12, %8, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %14, %15, %7, 1;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%19];\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%10], %5, %8, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%13], %12, %8, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%16], %15, %8, 1;\n\t"
             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%17];\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%18];\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%19];\n\t}" ::"r"(acc),
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%18];\n\t}" ::"r"(acc),
             "r"(acc + 64), "l"(xd), "r"(alo), "l"(wd), "l"(wd + 2), "r"(kc), "r"(id128), "r"(id64),
             "l"(xd + 2), "r"(alo + 8), "l"(xd + 4), "l"(wd + 4), "r"(alo + 16), "l"(xd + 6), "l"(wd + 6),
             "r"(alo + 24), "r"(smem_u32(&wempty[s])), "r"(smem_u32(&a_empty[a])), "r"(smem_u32(&empty[sx]))
@@ -436,7 +447,8 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
         uint32_t lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+          const float4 v = (mode & 128) ? make_float4(r * 1.5f, c * 1.25f, kc * 0.5f, 1.0f)
+                                        : *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int t = 0; t < 4; ++t)
@@ -485,15 +497,309 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   }
 }
 
-// W (n_cls x d float64) -> stacked [tf32(w32); w32 - tf32(w32)] (128 x d float32), zero padded.
+// ================================================================================================
+// CTA-pair version (cta_group::2, the default for >= 256 rows): two SMs of a TPC score a 256-row
+// pair tile with one M=256 MMA stream issued by the leader CTA. Each CTA keeps its own 128 X rows
+// (A operand: x_hi read by the tensor core straight from the TMA tile, x_lo from its TMEM) and
+// HALF of the classifier operand: per chunk a 96-row W tile = its 64-row half of [w_hi; w_lo]
+// (N=128 MMA) + its 32-row half of w_hi (N=64 MMA). Against the single-CTA kernel this halves the
+// tensor core's shared-memory reads of W (24 -> 12 KB per chunk) and the W tile writes
+// (16 -> 12 KB), which is what bounded it, and halves the MMA instructions per SM.
+//   leader (rank 0): MMA issue; its barriers collect the peer's TMA bytes (W), the peer's split
+//   arrivals (a_full) and the peer's epilogue arrivals (tmem_empty)
+//   MMA commits are multicast to the same barrier in both CTAs
+// ================================================================================================
+constexpr int kW2Rows = 96;
+constexpr int kTileW2 = kW2Rows * kKC * 4;  // 12 KB
+#ifndef OTF_MULTI2_X
+#define OTF_MULTI2_X 8
+#endif
+#ifndef OTF_MULTI2_W
+#define OTF_MULTI2_W 6
+#endif
+constexpr int kX2Stages = OTF_MULTI2_X;
+constexpr int kW2Stages = OTF_MULTI2_W;
+constexpr int kRing2Bytes = kX2Stages * kTileX + kW2Stages * kTileW2;  // 200 KB
+constexpr int kA2Slots = 8;                 // 32-column x_lo slots after 2 x 128 accumulator columns
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank0(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ bool mbar_try_cl(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
+  while (!mbar_try_cl(b, parity)) {
+  }
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t caddr) {
+#ifdef OTF_MULTI_REL_CLUSTER
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+#endif
+}
+
+// barriers that only see local arrivals or the leader's multicast commits
+#ifdef OTF_MULTI_CL_ALL
+#define OTF_WAIT_LOCAL mbar_wait_cl
+#else
+#define OTF_WAIT_LOCAL mbar_wait
+#endif
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMultiThreads, 1)
+multi_score_tc2(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                int64_t n, int d, int n_cls, float* __restrict__ out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kX2Stages], empty[kX2Stages];    // local X ring (empty: 4 split warps + commit)
+  __shared__ uint64_t wfull[kW2Stages], wempty[kW2Stages];  // wfull: leader's, both CTAs' bytes
+  __shared__ uint64_t a_full[kA2Slots], a_empty[kA2Slots];  // a_full: leader's, 8 split warps
+  __shared__ uint64_t tmem_full[2], tmem_empty[2];          // tmem_empty: leader's, 8 epilogue warps
+  __shared__ uint32_t tmem_base_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int64_t n_pt = (n + 2 * kMT - 1) / (2 * kMT);
+  const int kchunks = d / kKC;
+  unsigned char* const xring = smem;
+  unsigned char* const wring = smem + kX2Stages * kTileX;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kX2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 5);
+    }
+    for (int s = 0; s < kW2Stages; ++s) {
+      mbar_init(&wfull[s], 2);   // one expect_tx arrival per CTA
+      mbar_init(&wempty[s], 1);
+    }
+    for (int a = 0; a < kA2Slots; ++a) {
+      mbar_init(&a_full[a], 8);
+      mbar_init(&a_empty[a], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrival
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = tmem_base_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: this CTA's 128 X rows of each pair tile ----------------
+    uint32_t it = 0;
+    for (int64_t pt = pair; pt < n_pt; pt += npairs) {
+      const int row0 = (int)(pt * 2 * kMT + rank * kMT);
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % kX2Stages;
+        OTF_WAIT_LOCAL(&empty[s], ((it / kX2Stages) & 1u) ^ 1u);
+        tma_load_elect(xring + s * kTileX, &map_x, &full[s], kTileX, kc * kKC, row0);
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------- TMA producer: this CTA's W half, bytes counted on the leader's barrier ------
+    uint32_t it = 0;
+    for (int64_t pt = pair; pt < n_pt; pt += npairs) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % kW2Stages;
+        OTF_WAIT_LOCAL(&wempty[s], ((it / kW2Stages) & 1u) ^ 1u);
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%2], %3;\n\t"
+            "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%4, %5}], [%2];\n\t}" ::"r"(smem_u32(wring + s * kTileW2)),
+            "l"(&map_w), "r"(mapa_rank0(&wfull[s])), "r"((uint32_t)kTileW2), "r"(0),
+            "r"((int)((kc * 2 + (int)rank) * kW2Rows))
+            : "memory");
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (rank == 0) {
+      constexpr uint32_t id128 = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((256u >> 4) << 24);
+      constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((256u >> 4) << 24);
+      const uint64_t wdesc0 = umma_desc_sw128(smem_u32(wring));
+      const uint64_t xdesc0 = umma_desc_sw128(smem_u32(xring));
+      uint32_t it = 0, j = 0;
+      for (int64_t pt = pair; pt < n_pt; pt += npairs, ++j) {
+        const int b = j & 1;
+        mbar_wait_cl(&tmem_empty[b], ((j >> 1) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem_base + b * 128;
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const int s = it % kW2Stages, sx = it % kX2Stages, a = it % kA2Slots;
+          mbar_wait_cl(&wfull[s], (it / kW2Stages) & 1u);   // both W halves landed
+          mbar_wait_cl(&a_full[a], (it / kA2Slots) & 1u);   // both CTAs: X landed, x_lo in TMEM
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint64_t wd = wdesc0 + (uint64_t)((s * kTileW2) >> 4);
+          const uint64_t wd2 = wd + (uint64_t)((64 * 128) >> 4);  // rows 64..95: the w_hi half
+          const uint64_t xd = xdesc0 + (uint64_t)((sx * kTileX) >> 4);
+          const uint32_t alo = tmem_base + 256 + a * 32;
+          asm volatile(
+              "{\n\t.reg .pred e, p;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "setp.ne.b32 p, %5, 0;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %2, %4, %6, p;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %8, %9, %6, 1;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %10, %11, %6, 1;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %12, %13, %6, 1;\n\t"
+              "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%20], %23;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], [%3], %14, %7, 1;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], [%15], %16, %7, 1;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], [%17], %18, %7, 1;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], [%19], %24, %7, 1;\n\t"
+              "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%21], %23;\n\t"
+              "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%22], %23;\n\t}" ::"r"(acc),
+              "r"(acc + 64), "l"(xd), "r"(alo), "l"(wd), "r"(kc), "r"(id128), "r"(id64),
+              "l"(xd + 2), "l"(wd + 2), "l"(xd + 4), "l"(wd + 4), "l"(xd + 6), "l"(wd + 6),
+              "l"(wd2), "r"(alo + 8), "l"(wd2 + 2), "r"(alo + 16), "l"(wd2 + 4), "r"(alo + 24),
+              "r"(smem_u32(&empty[sx])), "r"(smem_u32(&wempty[s])), "r"(smem_u32(&a_empty[a])),
+              "h"((unsigned short)3), "l"(wd2 + 6)
+              : "memory");
+        }
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+                smem_u32(&tmem_full[b])),
+            "h"((unsigned short)3)
+            : "memory");
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- epilogue: this CTA's 128 rows ----------------
+    const int q = warp & 3;
+    const uint32_t te = mapa_rank0(&tmem_empty[0]);
+    uint32_t j = 0;
+    for (int64_t pt = pair; pt < n_pt; pt += npairs, ++j) {
+      const int b = j & 1;
+      OTF_WAIT_LOCAL(&tmem_full[b], (j >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int64_t row = pt * 2 * kMT + rank * kMT + 32 * q + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + b * 128;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t h[16], l[16];
+        tmem_ld16(taddr + c0, h);
+        tmem_ld16(taddr + 64 + c0, l);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < n) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int c = c0 + t;
+            if (c < n_cls) out[(int64_t)c * n + row] = __fadd_rn(__uint_as_float(h[t]), __uint_as_float(l[t]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(te + b * 8);
+    }
+  } else if (warp >= 8) {
+    // ---------------- split: x_lo of row r into this CTA's TMEM slot ----------------
+    const int q = warp & 3;
+    const uint32_t par = (uint32_t)((warp - 8) >> 2);
+    const int r = 32 * q + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const uint32_t af = mapa_rank0(&a_full[0]);
+    uint32_t it = 0;
+    for (int64_t pt = pair; pt < n_pt; pt += npairs) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        if ((it & 1u) != par) continue;
+        const int s = it % kX2Stages, a = it % kA2Slots;
+        OTF_WAIT_LOCAL(&full[s], (it / kX2Stages) & 1u);
+        const unsigned char* rowp = xring + s * kTileX + r * 128;
+        uint32_t lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            lo[4 * c + t] = __float_as_uint(__fsub_rn(e[t], __uint_as_float(__float_as_uint(e[t]) & 0xFFFFE000u)));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        OTF_WAIT_LOCAL(&a_empty[a], ((it / kA2Slots) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        tmem_st32(tmem_base + lane_off + 256 + a * 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(af + a * 8);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // no remote arrival or pair MMA may target a CTA that has left
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// W (n_cls x d float64) -> the CTA-pair layout: per chunk kc and CTA rank r a 96-row tile
+//   r = 0: rows 0..63 = w_hi[0..63],  rows 64..95 = w_hi[0..31]
+//   r = 1: rows 0..63 = w_lo[0..63],  rows 64..95 = w_hi[32..63]
+// stored [kc][r][96][32] (each tile one contiguous 12 KB block).
+__global__ void split_w2_kernel(const double* __restrict__ W, int n_cls, int d, float* __restrict__ ws) {
+  const int64_t total = (int64_t)64 * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / d), k = (int)(e % d);
+    const float w = c < n_cls ? __double2float_rn(W[e]) : 0.0f;
+    const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
+    const int64_t t0 = (int64_t)(k / kKC) * 2 * kW2Rows * kKC + (k % kKC);  // rank-0 tile of chunk
+    const int64_t t1 = t0 + (int64_t)kW2Rows * kKC;                          // rank-1 tile
+    ws[t0 + (int64_t)c * kKC] = hi;
+    ws[t1 + (int64_t)c * kKC] = __fsub_rn(w, hi);
+    if (c < 32) ws[t0 + (int64_t)(64 + c) * kKC] = hi;
+    else ws[t1 + (int64_t)(32 + c) * kKC] = hi;
+  }
+}
+
+// W (n_cls x d float64) -> stacked [tf32(w32); w32 - tf32(w32)] (128 x d float32, zero padded),
+// stored pre-tiled: tile kc (K columns 32kc .. 32kc+31 of all 128 rows) is one contiguous 16 KB
+// block, [kc][row][32], so every CTA's TMA of the shared W chunk reads 128 consecutive lines
+// (a row-major W would put the chunk's lines 4·d bytes apart, all hot in the same L2 slices).
 __global__ void split_w_kernel(const double* __restrict__ W, int n_cls, int d, float* __restrict__ ws) {
   const int64_t total = (int64_t)64 * d;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / d);
+    const int c = (int)(e / d), k = (int)(e % d);
     const float w = c < n_cls ? __double2float_rn(W[e]) : 0.0f;
     const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
-    ws[e] = hi;
-    ws[total + e] = __fsub_rn(w, hi);
+    const int64_t base = ((int64_t)(k / kKC) * 128) * kKC + (k % kKC);
+    ws[base + (int64_t)c * kKC] = hi;
+    ws[base + (int64_t)(64 + c) * kKC] = __fsub_rn(w, hi);
   }
 }
 
@@ -535,22 +841,41 @@ int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_
   if (n <= 0) return OTF_OK;
   if (n_cls < 1 || n_cls > 64) return fail(OTF_ERR_CONFIG, "multi-classifier scoring takes 1..64 classifiers");
   if (!multi_tc_supported(d, X)) return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs dim % 32 == 0");
-  split_w_kernel<<<64, 256, 0, st>>>(W, n_cls, d, ws);
-  OTF_LAUNCH_CHECK("split_w_kernel");
+  static const int mode = getenv("OTF_MULTI_MODE") ? atoi(getenv("OTF_MULTI_MODE")) : 0;
+  const int64_t tiles = (n + kMT - 1) / kMT;
+  const bool pair = tiles >= 2 && sm_count(device) >= 2 && !(mode & 256);
   CUtensorMap mx, mw;
   int rc = make_map(&mx, X, (uint64_t)d, (uint64_t)n, kMT);
-  if (!rc) rc = make_map(&mw, ws, (uint64_t)d, 128, 128);
   if (rc) return rc;
+  if (pair) {
+    split_w2_kernel<<<64, 256, 0, st>>>(W, n_cls, d, ws);
+    OTF_LAUNCH_CHECK("split_w2_kernel");
+    if ((rc = make_map(&mw, ws, (uint64_t)kKC, (uint64_t)(d / kKC) * 2 * kW2Rows, kW2Rows))) return rc;
+    const size_t smem = (size_t)kRing2Bytes + 1024;
+    static bool configured2[64] = {false};
+    if (!configured2[device & 63]) {
+      OTF_CUDA(cudaFuncSetAttribute((const void*)multi_score_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      configured2[device & 63] = true;
+    }
+    const int64_t pts = (tiles + 1) / 2;
+    int grid = sm_count(device) & ~1;
+    if (2 * pts < grid) grid = (int)(2 * pts);
+    multi_score_tc2<<<grid, kMultiThreads, smem, st>>>(mx, mw, n, d, n_cls, out);
+    OTF_LAUNCH_CHECK("multi_score_tc2");
+    return OTF_OK;
+  }
+  split_w_kernel<<<64, 256, 0, st>>>(W, n_cls, d, ws);
+  OTF_LAUNCH_CHECK("split_w_kernel");
+  if ((rc = make_map(&mw, ws, (uint64_t)kKC, (uint64_t)(d / kKC) * 128, 128))) return rc;
   const size_t smem = (size_t)kRingBytes + 1024;
   static bool configured[64] = {false};
   if (!configured[device & 63]) {
     OTF_CUDA(cudaFuncSetAttribute((const void*)multi_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[device & 63] = true;
   }
-  const int64_t tiles = (n + kMT - 1) / kMT;
   int grid = sm_count(device);
   if (tiles < grid) grid = (int)tiles;
-  static const int mode = getenv("OTF_MULTI_MODE") ? atoi(getenv("OTF_MULTI_MODE")) : 0;
   multi_score_tc<<<grid, kMultiThreads, smem, st>>>(mx, mw, n, d, n_cls, out, mode);
   OTF_LAUNCH_CHECK("multi_score_tc");
   return OTF_OK;
