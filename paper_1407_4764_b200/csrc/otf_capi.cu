@@ -481,6 +481,18 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
 
 // ---- many classifiers (C5b): tensor-core scoring of a dense repository ----------------------------
 namespace {
+// host W (n_cls x dim float64) -> pinned staging -> r->w (device), on st
+int stage_many(otf_repo* r, const double* W, int n_cls, cudaStream_t st, const double** dw) {
+  const size_t bytes = (size_t)n_cls * r->model_dim * sizeof(double);
+  int rc = r->h_w.ensure(bytes);
+  if (!rc) rc = r->w.ensure(bytes);
+  if (rc) return rc;
+  cudaStreamSynchronize(st);  // the staging buffer may still feed an earlier upload
+  std::memcpy(r->h_w.p, W, bytes);
+  OTF_CUDA(cudaMemcpyAsync(r->w.p, r->h_w.p, bytes, cudaMemcpyHostToDevice, st));
+  *dw = static_cast<const double*>(r->w.p);
+  return OTF_OK;
+}
 // scores for classifiers [c0, c0 + cn) into out (cn x n float32, classifier-major); W host/device.
 int multi_score_group(otf_repo* r, const double* dW, int cn, float* out, cudaStream_t st) {
   int rc = r->w32.ensure((size_t)multi_ws_floats(r->model_dim) * sizeof(float));
@@ -498,19 +510,15 @@ int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out,
   if (!multi_tc_supported(r->model_dim, static_cast<const float*>(r->payload)))
     return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs dim % 32 == 0");
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
-  const size_t wbytes = (size_t)n_cls * r->model_dim * sizeof(double);
-  DevBuf dW, dOut;
   const double* wp = W;
   int rc = OTF_OK;
-  if (mem == OTF_MEM_HOST) {
-    if ((rc = dW.ensure(wbytes))) return rc;
-    OTF_CUDA(cudaMemcpyAsync(dW.p, W, wbytes, cudaMemcpyHostToDevice, st));
-    wp = static_cast<const double*>(dW.p);
-    if ((rc = dOut.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
-  }
+  if (mem == OTF_MEM_HOST && (rc = stage_many(r, W, n_cls, st, &wp))) return rc;
+  if (mem == OTF_MEM_HOST &&
+      (rc = r->multi.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float))))
+    return rc;
   for (int c0 = 0; c0 < n_cls && !rc; c0 += 64) {
     const int cn = std::min(64, n_cls - c0);
-    float* o = mem == OTF_MEM_HOST ? static_cast<float*>(dOut.p) : out + (size_t)c0 * r->n;
+    float* o = mem == OTF_MEM_HOST ? static_cast<float*>(r->multi.p) : out + (size_t)c0 * r->n;
     rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, o, st);
     if (!rc && mem == OTF_MEM_HOST) {
       cudaError_t e = cudaMemcpyAsync(out + (size_t)c0 * r->n, o, (size_t)cn * r->n * sizeof(float),
@@ -519,7 +527,6 @@ int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out,
     }
   }
   if (mem == OTF_MEM_HOST || rc) cudaStreamSynchronize(st);
-  dW.release(); dOut.release();
   return rc;
 }
 
@@ -535,18 +542,15 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   if (out_n) *out_n = k_eff;
   if (k_eff == 0) return OTF_OK;
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
-  const size_t wbytes = (size_t)n_cls * r->model_dim * sizeof(double);
-  DevBuf dW, dIds, dSc;
   const double* wp = W;
   int rc = OTF_OK;
+  const size_t lbytes = (size_t)n_cls * k_eff * 8;  // ids (int64) and scores (float64) per list entry
   if (mem == OTF_MEM_HOST) {
-    if ((rc = dW.ensure(wbytes))) return rc;
-    OTF_CUDA(cudaMemcpyAsync(dW.p, W, wbytes, cudaMemcpyHostToDevice, st));
-    wp = static_cast<const double*>(dW.p);
-    if ((rc = dIds.ensure((size_t)n_cls * k_eff * 8)) || (rc = dSc.ensure((size_t)n_cls * k_eff * 8))) return rc;
+    if ((rc = stage_many(r, W, n_cls, st, &wp))) return rc;
+    if ((rc = r->outbuf.ensure(2 * lbytes)) || (rc = r->h_out.ensure(2 * lbytes))) return rc;
   }
-  int64_t* ids = mem == OTF_MEM_HOST ? static_cast<int64_t*>(dIds.p) : out_ids;
-  double* sc = mem == OTF_MEM_HOST ? static_cast<double*>(dSc.p) : out_scores;
+  int64_t* ids = mem == OTF_MEM_HOST ? static_cast<int64_t*>(r->outbuf.p) : out_ids;
+  double* sc = mem == OTF_MEM_HOST ? reinterpret_cast<double*>(static_cast<char*>(r->outbuf.p) + lbytes) : out_scores;
   // the (<= 64, n) score buffer is cached on the handle (2.56 GB for 64 x 10M rows)
   if ((rc = r->multi.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float)))) return rc;
   float* sbuf = static_cast<float*>(r->multi.p);
@@ -558,12 +562,15 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
                        ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff, nullptr, r->device, st);
   }
   if (!rc && mem == OTF_MEM_HOST) {
-    cudaError_t e = cudaMemcpyAsync(out_ids, ids, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(out_scores, sc, (size_t)n_cls * k_eff * 8, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
+    // one D2H of both arrays into pinned staging, then plain copies into the caller's buffers
+    cudaError_t e = cudaMemcpyAsync(r->h_out.p, r->outbuf.p, 2 * lbytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+    std::memcpy(out_ids, r->h_out.p, lbytes);
+    std::memcpy(out_scores, static_cast<char*>(r->h_out.p) + lbytes, lbytes);
+    return OTF_OK;
   }
-  if (mem == OTF_MEM_HOST || rc) cudaStreamSynchronize(st);
-  dW.release(); dIds.release(); dSc.release();
+  if (rc) cudaStreamSynchronize(st);
   return rc;
 }
 

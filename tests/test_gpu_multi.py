@@ -71,3 +71,22 @@ def test_multi_errors(otf):
     repo2 = otf.Repository.dense(otf.FeatureStore(np.ones((10, 64), np.float32)))
     with pytest.raises(otf.ConfigError):
         repo2.score_many([np.ones(32)])
+
+
+@pytest.mark.parametrize("n,d,c", [(1000, 128, 7), (300, 2048, 64)])
+def test_single_cta_path_matches_pair_path(otf, monkeypatch, n, d, c):
+    """The CTA-pair kernel (default) and the single-CTA kernel (inputs of one 128-row tile, forced
+    here with OTF_MULTI_SINGLE) both meet the TF32x3 bound and agree with each other."""
+    rng = np.random.default_rng(n * 7 + c)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    W = rng.standard_normal((c, d))
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    S_pair = repo.score_many(list(W))
+    monkeypatch.setenv("OTF_MULTI_SINGLE", "1")
+    S_single = repo.score_many(list(W))
+    monkeypatch.delenv("OTF_MULTI_SINGLE")
+    ex = exact(x, W).T
+    mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
+    for S in (S_pair, S_single):
+        assert np.all(np.abs(S - ex) <= 2.0 ** -18 * mag + np.spacing(np.abs(S)) + 1e-30)
+    assert np.all(np.abs(S_pair - S_single) <= 2.0 ** -17 * mag + 2 * np.spacing(np.abs(S_pair)) + 1e-30)
