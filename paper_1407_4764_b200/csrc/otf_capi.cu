@@ -117,6 +117,7 @@ struct otf_repo {
   DevBuf w, w32, lut, scores, bins, outbuf, multi;  // multi: (<=64, n) float32 classifier scores
   HostBuf h_w, h_out;
   TopkWs topk;
+  TopkWs mtopk;  // segment workspace of rank_many (kept apart: graphs capture topk's pointers)
   // graph cache for otf_repo_rank_graph
   cudaGraphExec_t gexec = nullptr;
   const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -206,6 +207,7 @@ void repo_free(otf_repo* r) {
   r->multi.release();
   r->h_w.release(); r->h_out.release();
   topk_ws_free(&r->topk);
+  topk_ws_free(&r->mtopk);
   if (r->stream) cudaStreamDestroy(r->stream);
   delete r;
 }
@@ -557,9 +559,15 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   for (int c0 = 0; c0 < n_cls && !rc; c0 += 64) {
     const int cn = std::min(64, n_cls - c0);
     rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, sbuf, st);
-    for (int c = 0; c < cn && !rc; ++c)
-      rc = launch_topk(sbuf + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base, k_eff, &r->topk, false,
-                       ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff, nullptr, r->device, st);
+    // all cn selections in one cooperative launch (a few SMs each) when the GPU has an SM pair
+    // per classifier; otherwise one launch per classifier over the whole GPU
+    if (!rc && sm_count(r->device) >= 2 * cn)
+      rc = launch_topk_segments(sbuf, cn, r->n, r->ids, r->id_base, k_eff, &r->mtopk,
+                                ids + (size_t)c0 * k_eff, sc + (size_t)c0 * k_eff, r->device, st);
+    else
+      for (int c = 0; c < cn && !rc; ++c)
+        rc = launch_topk(sbuf + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base, k_eff, &r->topk, false,
+                         ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff, nullptr, r->device, st);
   }
   if (!rc && mem == OTF_MEM_HOST) {
     // one D2H of both arrays into pinned staging, then plain copies into the caller's buffers

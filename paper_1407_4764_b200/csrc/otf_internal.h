@@ -49,9 +49,11 @@ struct TopkWs {
   uint64_t* key = nullptr;        // candidate order keys      (cap entries)
   uint64_t* inv = nullptr;        // candidate ~id             (cap entries)
   int64_t* row = nullptr;         // candidate row             (cap entries)
-  int64_t cap = 0;                // power of two >= max(k_eff, kCandCap)
+  int64_t cap = 0;                // power of two >= max(k_eff, kCandCap), per segment
+  int n_seg = 0;                  // segments the counters are laid out for
+  size_t slots = 0;               // allocated candidate slots (n_seg * cap)
 };
-int topk_ws_alloc(TopkWs* ws, int64_t k_eff);
+int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg = 1);
 void topk_ws_free(TopkWs* ws);
 // scores: float32 (dtype 0) or float64 (dtype 1), n entries on device. If hist_ready, ws->hist
 // already holds the coarse histogram of these scores (fused into the scoring kernel).
@@ -60,6 +62,11 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
                 int64_t* out_rows, int device, cudaStream_t st);
 // PQ rank path: per-row bins (+ fused histogram) from launch_pq_scan_bins; exact float64 scores
 // of candidates recomputed from codes + lut. scratch: n float64 (used only on the rare path).
+// n_seg independent top-k selections over consecutive float32 score arrays (scores + s*n) in one
+// cooperative launch (gridDim.x / n_seg CTAs each); outputs at out_ids/out_scores + s*k_eff.
+int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base,
+                         int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores, int device,
+                         cudaStream_t st);
 int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,
                         int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, TopkWs* ws,
                         double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows,

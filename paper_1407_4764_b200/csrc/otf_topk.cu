@@ -77,6 +77,7 @@ struct DirectSrc {
   using T = ST;
   static constexpr int kLoadBytes = sizeof(ST);
   const ST* s;
+  __device__ __forceinline__ void shift(int64_t o) { s += o; }
   __device__ __forceinline__ ST load(int64_t i) const { return __ldcg(s + i); }
   // 8 consecutive entries from i (i % 8 == 0): two float4 / four double2 loads.
   __device__ __forceinline__ void load8(int64_t i, ST (&v)[8]) const {
@@ -103,6 +104,7 @@ struct PqBinSrc {
   using T = double;
   static constexpr int kLoadBytes = 2;
   const uint16_t* bins; const uint8_t* codes; const double* lut; int M, K;
+  __device__ __forceinline__ void shift(int64_t) {}  // one segment only
   __device__ __forceinline__ uint32_t load(int64_t i) const { return __ldcg(bins + i); }
   __device__ __forceinline__ void load8(int64_t i, uint32_t (&v)[8]) const {
     const uint4 a = __ldcg(reinterpret_cast<const uint4*>(bins + i));
@@ -127,6 +129,20 @@ struct PqBinSrc {
   }
   __device__ __forceinline__ double out_score(int64_t, uint64_t key) const { return key_to_f64(key); }
 };
+
+// Workspace of segment `seg`: per segment one block of kWsWords counters (histogram, radix
+// histograms, barrier, count) and `cap` candidate slots.
+constexpr int64_t kWsWords = kHistBins + 3 * 256 + 4;
+__device__ __forceinline__ TopkWs seg_ws(TopkWs ws, unsigned seg) {
+  ws.hist += (int64_t)seg * kWsWords;
+  ws.rhist = ws.hist + kHistBins;
+  ws.bar = reinterpret_cast<unsigned int*>(ws.rhist + 3 * 256);
+  ws.count = ws.bar + 2;
+  ws.key += (int64_t)seg * ws.cap;
+  ws.inv += (int64_t)seg * ws.cap;
+  ws.row += (int64_t)seg * ws.cap;
+  return ws;
+}
 
 // Appends (key, ~id, row) for every lane with `take`, one atomic per warp.
 __device__ __forceinline__ void append_candidate(const TopkWs& ws, bool take, uint64_t key,
@@ -231,8 +247,8 @@ __device__ __forceinline__ void pick_bin256(const uint32_t* h, int64_t need, int
 template <typename Src>
 __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k_eff,
                           unsigned char* dyn, int64_t* out_ids, double* out_scores,
-                          int64_t* out_rows) {
-  const int64_t mine = m > blockIdx.x ? (m - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+                          int64_t* out_rows, unsigned vb, unsigned vnb) {
+  const int64_t mine = m > vb ? (m - 1 - vb) / vnb + 1 : 0;
   if (mine == 0) return;
   uint64_t* sk = reinterpret_cast<uint64_t*>(dyn);
   uint64_t* si = sk + m;
@@ -243,7 +259,7 @@ __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t q = wid; q < mine; q += nw) {
-    const int64_t i = blockIdx.x + q * gridDim.x;
+    const int64_t i = vb + q * vnb;
     const uint64_t ki = sk[i], ii = si[i];
     int64_t cnt = 0;
     for (int64_t j = lane; j < m; j += 32) cnt += cand_greater(sk[j], si[j], ki, ii);
@@ -263,13 +279,14 @@ template <typename ST, typename Src>
 __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, const int64_t* ids,
                                   int64_t id_base, int64_t k_eff, const TopkWs& ws, bool all,
                                   unsigned char* dyn, int64_t* out_ids, double* out_scores,
-                                  int64_t* out_rows, uint32_t* h, int* s_b, int64_t* s_above) {
+                                  int64_t* out_rows, uint32_t* h, int* s_b, int64_t* s_above, unsigned vb,
+                                  unsigned vnb) {
   constexpr int KB = KeyBits<ST>::value;
-  const unsigned int nb = gridDim.x;
+  const unsigned int nb = vnb;
   const int lane = threadIdx.x & 31;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const int64_t tid = (int64_t)vb * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)vnb * blockDim.x;
+  const int64_t wbase0 = (int64_t)vb * blockDim.x + (threadIdx.x & ~31);
   uint64_t pre = 0, msk = 0, pre2 = 0, msk2 = 0;
   int64_t need = k_eff;
   int phase = all ? 2 : 0;  // k_eff == n: everything is gathered (mask 0)
@@ -278,7 +295,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
   int it = 0;
   while (phase < 2) {
     uint32_t* H = ws.rhist + (it % 3) * 256;
-    if (blockIdx.x == 0 && threadIdx.x < 256) ws.rhist[((it + 1) % 3) * 256 + threadIdx.x] = 0u;
+    if (vb == 0 && threadIdx.x < 256) ws.rhist[((it + 1) % 3) * 256 + threadIdx.x] = 0u;
     if (threadIdx.x < 256) h[threadIdx.x] = 0u;
     __syncthreads();
     if (phase == 0) {
@@ -336,13 +353,13 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
     append_candidate(ws, in, key, inv, i, k_eff);
   }
   grid_barrier(ws.bar, nb);
-  if (blockIdx.x == 0) {
+  if (vb == 0) {
     for (int t = threadIdx.x; t < 3 * 256; t += blockDim.x) ws.rhist[t] = 0u;
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
   }
   if (k_eff <= kCandCap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *ws.count = 0u;
-    rank_emit(src, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows);
+    if (vb == 0 && threadIdx.x == 0) *ws.count = 0u;
+    rank_emit(src, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
     return;
   }
   // global bitonic sort over ws (capacity P)
@@ -384,17 +401,29 @@ __global__ void __launch_bounds__(kTopkThreads, kTopkCtasPerSm)
 topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id_base,
                  int64_t k_eff, TopkWs ws, int hist_ready, typename Src::T* scratch,
                  int64_t* __restrict__ out_ids, double* __restrict__ out_scores,
-                 int64_t* __restrict__ out_rows) {
+                 int64_t* __restrict__ out_rows, int n_seg) {
   using ST = typename Src::T;
+  // Segments (n_seg > 1, DirectSrc only): n_seg independent selections of k_eff out of n over
+  // consecutive score arrays (the multi-classifier path), each on its own gridDim.x / n_seg CTAs
+  // with its own workspace; vb / vnb are the CTA's index and count inside its segment.
+  const unsigned per = gridDim.x / (unsigned)n_seg;
+  const unsigned seg = blockIdx.x / per, vb = blockIdx.x % per, vnb = per;
+  if (n_seg > 1) {
+    src.shift((int64_t)seg * n);
+    scratch += (int64_t)seg * n;
+    out_ids += (int64_t)seg * k_eff;
+    out_scores += (int64_t)seg * k_eff;
+    ws = seg_ws(ws, seg);
+  }
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ uint32_t h[256];
   __shared__ int s_b;
   __shared__ int64_t s_above, s_cnt;
   __shared__ int64_t wsum[32];
-  const unsigned int nb = gridDim.x;
+  const unsigned int nb = vnb;
   const int lane = threadIdx.x & 31;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const int64_t nthreads = (int64_t)vnb * blockDim.x;
+  const int64_t wbase0 = (int64_t)vb * blockDim.x + (threadIdx.x & ~31);
   const bool all = k_eff >= n;
 
   // ---- A: coarse histogram (skipped when fused into the scoring kernel) --------------------
@@ -467,43 +496,50 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
       }
     }
     grid_barrier(ws.bar, nb);
-    if (blockIdx.x == 0) {  // every CTA has read hist and count is no longer needed
+    if (vb == 0) {  // every CTA has read hist and count is no longer needed
       for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
-    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows);
+    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
     return;
   }
 
   // ---- D: exact radix select over a materialised score array --------------------------------
   const ST* scores = scratch;
   if (Src::kLoadBytes == 2) {  // bins-only source: compute every exact score once
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthreads)
+    for (int64_t i = (int64_t)vb * blockDim.x + threadIdx.x; i < n; i += nthreads)
       scratch[i] = src.exact(i, src.load(i));
     grid_barrier(ws.bar, nb);
   }
   radix_select_emit(scores, src, n, ids, id_base, k_eff, ws, all, dyn, out_ids, out_scores, out_rows,
-                    h, &s_b, &s_above);
+                    h, &s_b, &s_above, vb, vnb);
 }
 
-int topk_ws_alloc(TopkWs* ws, int64_t k_eff) {
+int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg) {
   int64_t P = kCandCap;
   while (P < k_eff) P <<= 1;
-  if (ws->hist == nullptr) {
-    const size_t bytes = (kHistBins + 3 * 256 + 4) * sizeof(uint32_t);
+  if (n_seg > ws->n_seg) {
+    cudaFree(ws->hist);
+    ws->hist = nullptr;
+    ws->n_seg = 0;
+    const size_t bytes = (size_t)n_seg * kWsWords * sizeof(uint32_t);
     OTF_CUDA(cudaMalloc(&ws->hist, bytes));
     OTF_CUDA(cudaMemset(ws->hist, 0, bytes));
     ws->rhist = ws->hist + kHistBins;
     ws->bar = reinterpret_cast<unsigned int*>(ws->rhist + 3 * 256);
     ws->count = ws->bar + 2;
+    ws->n_seg = n_seg;
+    ws->cap = 0;  // re-layout the candidate arrays for the new segment count
   }
-  if (P > ws->cap) {
+  if (P > ws->cap || (size_t)ws->n_seg * P > ws->slots) {
     cudaFree(ws->key); cudaFree(ws->inv); cudaFree(ws->row);
-    ws->key = nullptr; ws->inv = nullptr; ws->row = nullptr; ws->cap = 0;
-    OTF_CUDA(cudaMalloc(&ws->key, P * sizeof(uint64_t)));
-    OTF_CUDA(cudaMalloc(&ws->inv, P * sizeof(uint64_t)));
-    OTF_CUDA(cudaMalloc(&ws->row, P * sizeof(int64_t)));
+    ws->key = nullptr; ws->inv = nullptr; ws->row = nullptr; ws->cap = 0; ws->slots = 0;
+    const size_t slots = (size_t)ws->n_seg * P;
+    OTF_CUDA(cudaMalloc(&ws->key, slots * sizeof(uint64_t)));
+    OTF_CUDA(cudaMalloc(&ws->inv, slots * sizeof(uint64_t)));
+    OTF_CUDA(cudaMalloc(&ws->row, slots * sizeof(int64_t)));
     ws->cap = P;
+    ws->slots = slots;
   }
   return OTF_OK;
 }
@@ -516,7 +552,7 @@ void topk_ws_free(TopkWs* ws) {
 template <typename Src>
 static int launch_src(const Src& src, int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff,
                       TopkWs* ws, bool hist_ready, typename Src::T* scratch, int64_t* out_ids,
-                      double* out_scores, int64_t* out_rows, int device, cudaStream_t st) {
+                      double* out_scores, int64_t* out_rows, int device, cudaStream_t st, int n_seg = 1) {
   auto fn = topk_coop_kernel<Src>;
   static bool configured[64] = {false};
   if (!configured[device & 63]) {
@@ -524,9 +560,11 @@ static int launch_src(const Src& src, int64_t n, const int64_t* ids, int64_t id_
                                   (int)kTopkSmem));
     configured[device & 63] = true;
   }
-  int grid = sm_count(device) * kTopkCtasPerSm;
+  int per = sm_count(device) * kTopkCtasPerSm / n_seg;  // CTAs per segment
+  if (per < 1) return fail(OTF_ERR_CONFIG, "more top-k segments than SMs");
   const int64_t useful = (n + kTopkThreads - 1) / kTopkThreads;
-  if (useful < grid) grid = (int)(useful > 0 ? useful : 1);
+  if (useful < per) per = (int)(useful > 0 ? useful : 1);
+  const int grid = per * n_seg;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTopkThreads);
@@ -538,7 +576,7 @@ static int launch_src(const Src& src, int64_t n, const int64_t* ids, int64_t id_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, src, n, ids, id_base, k_eff, *ws, (int)hist_ready, scratch,
-                              out_ids, out_scores, out_rows));
+                              out_ids, out_scores, out_rows, n_seg));
   count_launch();
   return OTF_OK;
 }
@@ -557,6 +595,19 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
   DirectSrc<double> src{static_cast<const double*>(scores)};
   return launch_src(src, n, ids, id_base, k_eff, ws, hist_ready, const_cast<double*>(src.s), out_ids,
                     out_scores, out_rows, device, st);
+}
+
+// n_seg independent top-k selections over consecutive float32 score arrays (scores + s*n), one
+// cooperative launch; outputs at out_ids/out_scores + s*k_eff. ws must be a segment workspace.
+int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base,
+                         int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores, int device,
+                         cudaStream_t st) {
+  if (k_eff <= 0 || n <= 0 || n_seg <= 0) return OTF_OK;
+  int rc = topk_ws_alloc(ws, k_eff, n_seg);
+  if (rc) return rc;
+  DirectSrc<float> src{scores};
+  return launch_src(src, n, ids, id_base, k_eff, ws, false, const_cast<float*>(scores), out_ids, out_scores,
+                    nullptr, device, st, n_seg);
 }
 
 int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,

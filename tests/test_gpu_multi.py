@@ -90,3 +90,28 @@ def test_single_cta_path_matches_pair_path(otf, monkeypatch, n, d, c):
     for S in (S_pair, S_single):
         assert np.all(np.abs(S - ex) <= 2.0 ** -18 * mag + np.spacing(np.abs(S)) + 1e-30)
     assert np.all(np.abs(S_pair - S_single) <= 2.0 ** -17 * mag + 2 * np.spacing(np.abs(S_pair)) + 1e-30)
+
+
+@pytest.mark.parametrize("n,d,c,k", [(50_000, 64, 64, 1000), (3000, 32, 40, 3000), (9000, 96, 5, 8500),
+                                     (4000, 64, 70, 50), (600, 32, 130, 17)])
+def test_rank_many_segmented_topk(otf, n, d, c, k):
+    """rank_many selects all classifiers of a group in one segmented cooperative launch (two or
+    more SMs per classifier); lists equal the oracle's top_k of the scores, including heavy ties
+    (zero and constant classifiers -> the radix-select path), k > the 8192-candidate cap, k == n,
+    and groups too large for one launch (per-classifier fallback; > 64 classifiers = 2 groups)."""
+    rng = np.random.default_rng(n + c + k)
+    x = np.round(rng.standard_normal((n, d)) * 4).astype(np.float32) / 4  # many exact ties
+    ids = rng.permutation(4 * n)[:n].astype(np.int64)
+    W = rng.standard_normal((c, d))
+    W[0] = 0.0                 # all scores 0: one giant tie
+    W[c // 2] = np.round(W[c // 2])
+    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    S = repo.score_many(list(W))
+    lists = repo.rank_many([otf.LinearModel(w, 1, 1) for w in W], k)
+    for i in range(c):
+        o_ids, o_sc, _ = O.top_k(S[i], k, ids)
+        np.testing.assert_array_equal(lists[i].ids, o_ids)
+        np.testing.assert_array_equal(lists[i].scores, o_sc)
+    # the single-classifier ranking of the same repository is unaffected (separate workspace)
+    r1 = repo.rank(otf.LinearModel(W[1], 1, 1), k)
+    assert len(r1.ids) == min(k, n)
