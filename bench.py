@@ -42,8 +42,9 @@ CONFIGS = {
                workload="C1: 1M x 128-D fp32 features per GPU, single-query linear-SVM score + exact top-1000",
                # PAPER.md:751-752 (GTX Titan): score 1M CNN-128 features ~0.01 s + rank ~0.002 s
                published=1_000_000 / 0.012),
-    "c4": dict(kind="dense", rows=6_250_000, dim=2048, k=1000,
-               workload="C4: 6.25M x 2048-D fp32 rows per GPU (50M over 8 GPUs), score + top-1000 + NCCL merge"),
+    "c4": dict(kind="dense", rows=6_250_000, dim=2048, k=1000, train=True,
+               workload="C4: 6.25M x 2048-D fp32 rows per GPU (50M over 8 GPUs), score + top-1000 + NCCL merge, "
+                        "Pegasos training concurrent with ranking (rank 0, own stream)"),
     "c3": dict(kind="pq", rows=10_000_000, dim=16, k=1000, subdim=8,
                workload="C3: 10M PQ codes per GPU (16 sub-quantizers x 256 centroids, 128-D), LUT score + top-1000"),
     "c5a": dict(kind="binary", rows=100_000_000, dim=2048, k=1000,
@@ -246,6 +247,51 @@ def make_repository(cfg, rank, world, device, seed=20260418):
     return repo, keep, start
 
 
+class ConcurrentTrainer:
+    """Pegasos steps in a background thread while the ranking steps are timed (C4: "SGD training
+    concurrent with ranking"). The trainer (the package's OnlineTrainer: 16 384 fixed negatives,
+    200 positives in its device pool, batch 32) launches on its own high-priority stream; ctypes
+    releases the GIL, so its steps interleave with the ranking launches of the main thread."""
+
+    def __init__(self, dim, device):
+        import threading
+
+        from paper_1407_4764_b200.trainer import OnlineTrainer, TrainerConfig
+
+        rng = np.random.default_rng(7)
+        neg = rng.standard_normal((16_384, dim)).astype(np.float32)
+        neg /= np.linalg.norm(neg, axis=1, keepdims=True)
+        pos = rng.standard_normal((200, dim)).astype(np.float32) + 0.5
+        pos /= np.linalg.norm(pos, axis=1, keepdims=True)
+        self.cfg = TrainerConfig(lam=1e-3, batch_size=32, seed=3)
+        self.tr = OnlineTrainer(dim, neg, self.cfg, device=device)
+        self.tr.append_positives(pos)
+        self.steps = 0
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            self.tr.step()
+            self.steps += 1
+
+    def start(self):
+        self._th.start()
+
+    def mark(self):
+        return self.steps, time.perf_counter()
+
+    def stop(self, m0, m1):
+        self._stop.set()
+        self._th.join()
+        steps = m1[0] - m0[0]
+        secs = max(m1[1] - m0[1], 1e-9)
+        return {"concurrent": True, "trainer_steps_in_timed_region": int(steps),
+                "trainer_steps_per_s": steps / secs, "batch": self.cfg.batch_size, "negatives": 16_384,
+                "positives": 200, "where": "rank 0, OnlineTrainer on its own high-priority stream",
+                "final_iteration": int(self.tr.iteration)}
+
+
 def run_gpu(args, cfg):
     import torch
     import torch.distributed as dist
@@ -310,6 +356,11 @@ def run_gpu(args, cfg):
         if world > 1:
             dist.barrier()
 
+    train_on = cfg.get("train", False) if args.train is None else args.train
+    trainer = ConcurrentTrainer(dim, local) if train_on and rank == 0 else None
+    if trainer:
+        trainer.start()
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -320,6 +371,7 @@ def run_gpu(args, cfg):
     launches0 = _lib.launch_count()
     barrier()
     torch.cuda.synchronize(dev)
+    t_mark0 = trainer.mark() if trainer else None
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             if flush:
@@ -328,6 +380,7 @@ def run_gpu(args, cfg):
             step()
             ends[i].record(stream)
         torch.cuda.synchronize(dev)
+    t_mark1 = trainer.mark() if trainer else None
     barrier()
     launches = _lib.launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -394,6 +447,7 @@ def run_gpu(args, cfg):
         api()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_t))
+    training = trainer.stop(t_mark0, t_mark1) if trainer else None
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -444,6 +498,8 @@ def run_gpu(args, cfg):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if training:
+            line["training"] = training
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -459,6 +515,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--train", dest="train", action="store_true", default=None,
+                    help="run Pegasos steps concurrently with ranking (default: on for c4 only)")
+    ap.add_argument("--no-train", dest="train", action="store_false")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if os.environ.get("OTF_BENCH_ROWS"):  # profiling runs only: shrink the repository

@@ -56,6 +56,8 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint8_t* base = codes + (int64_t)slice * 128 + 4 * lane;
   constexpr int R = 32;  // rows per warp iteration
+  bool writer;
+  const int slot = row_of_lane<R, 32>(lane, &writer);  // the row this lane finishes
   for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
     uint32_t wd[R];
     const uint8_t* rp = base + r0 * RB;
@@ -67,6 +69,10 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
       for (int i = 0; i < R; ++i)
         wd[i] = r0 + i < n ? __ldcs(reinterpret_cast<const uint32_t*>(rp + i * RB)) : 0u;
     }
+    const int64_t row = r0 + slot;
+    const bool active = writer && row < n;
+    // the previous slice's partial is loaded with the codes (its latency was exposed at the end)
+    const double pin = active && partial_in ? __ldcs(partial_in + row) : 0.0;
     float p[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -78,12 +84,8 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
       p[i] = s;
     }
     transposed_reduce_f<R, 32>(p, lane);
-    bool writer;
-    const int slot = row_of_lane<R, 32>(lane, &writer);
-    const int64_t row = r0 + slot;
-    const bool active = writer && row < n;
     double total = (double)p[0];
-    if (active && partial_in) total = __dadd_rn(__ldcs(partial_in + row), total);
+    if (active && partial_in) total = __dadd_rn(pin, total);
     if (out) {
       const float sc = __double2float_rn(total);
       if (active) out[row] = sc;
