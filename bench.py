@@ -335,6 +335,14 @@ def run_gpu(args, cfg):
         def step():
             _lib.check(lib.otf_repo_rank_many(repo.handle, _lib.tptr(W_dev), n_cls, k, _lib.tptr(m_ids),
                                               _lib.tptr(m_sc), C.byref(m_got), _lib.MEM_DEVICE, sp))
+    elif world > 1 and args.group == "native":
+        # the library's own NCCL communicator (otf_group_*); the unique id travels over torch
+        from paper_1407_4764_b200.distributed import NcclShardGroup
+
+        uid = [NcclShardGroup.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sharded = NcclShardGroup(repo, uid[0], world, rank, start, total_rows)
+        step = lambda: sharded.rank_device(w_dev, k)
     elif world > 1:
         sharded = ShardedRepository.from_local(repo, total_rows, start)
         step = lambda: sharded.rank_device(w_dev, k)
@@ -429,6 +437,8 @@ def run_gpu(args, cfg):
     if multi:
         models = [otf.LinearModel(wc, 1, 1) for wc in Wm]
         api = lambda: repo.rank_many(models, k)
+    elif world > 1 and args.group == "native":
+        api = lambda: sharded.rank(model, k)
     elif world > 1:
         api = lambda: sharded.rank(model, k, root_only=True)
     else:
@@ -483,7 +493,7 @@ def run_gpu(args, cfg):
                       "multi": "f32 via tcgen05 tf32x3"}[cfg["kind"]],
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "rows_per_gpu": n_local, "total_rows": total_rows,
-                       "dim_or_blocks_or_bits": cfg["dim"], "k": k, "parallelism": f"dp{world} (rows sharded)",
+                       "dim_or_blocks_or_bits": cfg["dim"], "k": k, "parallelism": f"dp{world} (rows sharded)", "exchange": (args.group if world > 1 else "none"),
                        "l2": ("L2 flushed between timed steps" if flush else
                               f"inputs ({payload / 1e9:.1f} GB/GPU) larger than L2")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -518,6 +528,9 @@ def main():
     ap.add_argument("--train", dest="train", action="store_true", default=None,
                     help="run Pegasos steps concurrently with ranking (default: on for c4 only)")
     ap.add_argument("--no-train", dest="train", action="store_false")
+    ap.add_argument("--group", choices=["torch", "native"], default="torch",
+                    help="N>1 exchange: torch.distributed NCCL collectives (default) or the library's own "
+                         "NCCL communicator (otf_group_*)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if os.environ.get("OTF_BENCH_ROWS"):  # profiling runs only: shrink the repository

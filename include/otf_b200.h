@@ -208,6 +208,28 @@ int otf_trainer_weights_ptr(otf_trainer* tr, const double** out);
 /* The trainer's CUDA stream (high priority; runs concurrently with ranking). */
 int otf_trainer_stream(otf_trainer* tr, void** out);
 
+/* ---- multi-GPU group (one process per GPU, shards by image) ------------
+ * A native NCCL communicator over the ranks' shard handles. NCCL is loaded at run time
+ * (libnccl.so.2, the one torch already mapped if any), so the library itself has no link-time
+ * NCCL dependency. Per query: ncclBroadcast of w from `root`, the local exact top-k of this
+ * rank's shard (otf_repo_rank), ncclAllGather of k x (float64 score, int64 id, int64 global row)
+ * (ranks with fewer than k rows pad with (-inf, 2^62 + rank*k + slot, -1)), then the exact
+ * (-score, id) top-k of the gathered candidates on every rank. Ids must be unique across ranks;
+ * row scores do not depend on the shard, so results equal a single-GPU rank of all rows.
+ * Replaces: the single-process Repository.rank (ranker.py:272-281) at 1/2/4/8 GPUs. */
+typedef struct otf_group otf_group;
+/* 128-byte ncclUniqueId of a new communicator (rank 0 creates it, the caller distributes it). */
+int otf_group_unique_id(unsigned char id[128]);
+int otf_group_create(int device, int32_t n_ranks, int32_t rank, const unsigned char id[128], otf_group** out);
+int otf_group_destroy(otf_group* g);
+/* w: model_dim float64 on `root` (host or device per mem; ignored elsewhere). shard: this rank's
+ * repository, its rows are global rows row_offset .. row_offset + count - 1. total_rows: the sum
+ * of all shards (k_eff = min(k, total_rows)). Outputs (k_eff entries, every rank): ids, float64
+ * scores, global rows (nullable). */
+int otf_group_rank(otf_group* g, otf_repo* shard, const double* w, int32_t root, int64_t row_offset,
+                   int64_t total_rows, int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+                   int64_t* out_n, int mem, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ LIB = PKG / "libotf_b200.so"
 OBJ = PKG / "build"
 
 SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu", "otf_multi.cu",
-           "otf_batch.cu"]
+           "otf_batch.cu", "otf_group.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = LIB.with_suffix(".so.tmp")
     link = [cc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *map(str, objs),
-            "-lcudart"]
+            "-lcudart", "-ldl"]
     subprocess.run(link, check=True)
     os.replace(tmp, LIB)
     return LIB

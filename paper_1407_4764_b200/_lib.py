@@ -85,6 +85,10 @@ SIGNATURES: dict[str, list] = {
     "otf_trainer_set_weights": [_vp, _vp, _int],
     "otf_trainer_weights_ptr": [_vp, _P(_vp)],
     "otf_trainer_stream": [_vp, _P(_vp)],
+    "otf_group_unique_id": [_vp],
+    "otf_group_create": [_int, _i32, _i32, _vp, _P(_vp)],
+    "otf_group_destroy": [_vp],
+    "otf_group_rank": [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _P(_i64), _int, _vp],
 }
 _RESTYPE = {"otf_last_error": C.c_char_p, "otf_kernel_names": C.c_char_p, "otf_launch_count": _i64}
 

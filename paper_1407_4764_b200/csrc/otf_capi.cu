@@ -291,10 +291,10 @@ int otf_abi_version(void) { return 1; }
 int64_t otf_launch_count(void) { return g_launches.load(); }
 
 const char* otf_kernel_names(void) {
-  return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;"
-         "pq_scan_generic;pq_check_codes;bin_score_fast;bin_score_generic;"
-         "bin_unpack;bin_binarize;bin_hamming;topk_coop_kernel;pegasos_kernel;gather_rows_kernel;"
-         "gather_i64_kernel";
+  return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;pq_scan16_xor;"
+         "pq_scan_generic;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
+         "bin_hamming;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
+         "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local";
 }
 
 int otf_device_count(int* out) {
@@ -1018,3 +1018,120 @@ int otf_trainer_stream(otf_trainer* t, void** out) {
 }
 
 }  // extern "C"
+
+// ---- multi-GPU group (otf_group.cu) ---------------------------------------------------------------
+struct otf_group {
+  int device = 0;
+  int n_ranks = 1, rank = 0;
+  void* comm = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf w, loc, all, outbuf;  // w (dim f64); local k x (sc, id, row); gathered; merged output
+  HostBuf h_w, h_out;
+  TopkWs topk;
+};
+
+int otf_group_unique_id(unsigned char id[128]) { return group_unique_id(id); }
+
+int otf_group_create(int device, int32_t n_ranks, int32_t rank, const unsigned char id[128], otf_group** out) {
+  if (!out) return fail(OTF_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(OTF_ERR_CONFIG, "rank out of range");
+  int ndev = 0;
+  int rc = otf_device_count(&ndev);
+  if (rc) return rc;
+  if (device < 0 || device >= ndev) return fail(OTF_ERR_CONFIG, "device out of range");
+  DeviceGuard g(device);
+  otf_group* grp = new otf_group();
+  grp->device = device;
+  grp->n_ranks = n_ranks;
+  grp->rank = rank;
+  if ((rc = group_comm_create(n_ranks, rank, id, &grp->comm))) { delete grp; return rc; }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaStreamCreateWithPriority(&grp->stream, cudaStreamNonBlocking, lo) != cudaSuccess) {
+    group_comm_destroy(grp->comm);
+    delete grp;
+    return fail(OTF_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  *out = grp;
+  return OTF_OK;
+}
+
+int otf_group_destroy(otf_group* g) {
+  if (!g) return OTF_OK;
+  DeviceGuard dg(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  group_comm_destroy(g->comm);
+  g->w.release(); g->loc.release(); g->all.release(); g->outbuf.release();
+  g->h_w.release(); g->h_out.release();
+  topk_ws_free(&g->topk);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+  return OTF_OK;
+}
+
+int otf_group_rank(otf_group* g, otf_repo* r, const double* w, int32_t root, int64_t row_offset, int64_t total_rows,
+                   int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
+                   void* stream) {
+  if (!g || !r) return fail(OTF_ERR_CONFIG, "group or shard is NULL");
+  if (r->device != g->device) return fail(OTF_ERR_CONFIG, "shard and group are on different devices");
+  if (root < 0 || root >= g->n_ranks) return fail(OTF_ERR_CONFIG, "root out of range");
+  std::lock_guard<std::mutex> lg(g->mu);
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard dg(g->device);
+  const int64_t k_eff = k < 0 ? 0 : (k > total_rows ? total_rows : k);
+  if (out_n) *out_n = k_eff;
+  if (k_eff == 0) return OTF_OK;
+  cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(g->stream, stream) : g->stream;
+  const int64_t d = r->model_dim, P = g->n_ranks;
+  int rc = OTF_OK;
+  if ((rc = g->w.ensure((size_t)d * 8)) || (rc = g->loc.ensure((size_t)k_eff * 24)) ||
+      (rc = g->all.ensure((size_t)P * k_eff * 24)) || (rc = g->outbuf.ensure((size_t)k_eff * 32)))
+    return rc;
+  double* dw = static_cast<double*>(g->w.p);
+  // 1. broadcast w from root
+  if (g->rank == root) {
+    if (mem == OTF_MEM_HOST) {
+      if ((rc = g->h_w.ensure((size_t)d * 8))) return rc;
+      std::memcpy(g->h_w.p, w, (size_t)d * 8);
+      OTF_CUDA(cudaMemcpyAsync(dw, g->h_w.p, (size_t)d * 8, cudaMemcpyHostToDevice, st));
+    } else {
+      OTF_CUDA(cudaMemcpyAsync(dw, w, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if ((rc = group_broadcast_f64(g->comm, dw, d, root, st))) return rc;
+  // 2. local exact top-k of the shard, in exchange format (global rows, pads)
+  double* lsc = static_cast<double*>(g->loc.p);
+  int64_t* lid = reinterpret_cast<int64_t*>(lsc + k_eff);
+  int64_t* lrow = lid + k_eff;
+  const int64_t k_loc = std::min<int64_t>(k_eff, r->n);
+  if (k_loc > 0 && (rc = rank_device(r, dw, k_loc, lid, lsc, lrow, st))) return rc;
+  if ((rc = launch_group_finalize(lsc, lid, lrow, k_loc, k_eff, row_offset,
+                                  (int64_t(1) << 62) + (int64_t)g->rank * k_eff, st)))
+    return rc;
+  // 3. allgather the candidates of every rank
+  double* asc = static_cast<double*>(g->all.p);
+  int64_t* aid = reinterpret_cast<int64_t*>(asc + P * k_eff);
+  int64_t* arow = aid + P * k_eff;
+  if ((rc = group_allgather_candidates(g->comm, lsc, lid, lrow, k_eff, asc, aid, arow, st))) return rc;
+  // 4. exact merge: top-k by (-score, id) of the P*k candidates, then their global rows
+  int64_t* mids = static_cast<int64_t*>(g->outbuf.p);
+  double* msc = reinterpret_cast<double*>(mids + k_eff);
+  int64_t* mpos = reinterpret_cast<int64_t*>(msc + k_eff);
+  int64_t* mrow = mpos + k_eff;
+  const bool dev = mem == OTF_MEM_DEVICE;
+  if ((rc = launch_topk(asc, OTF_F64, P * k_eff, aid, 0, k_eff, &g->topk, false, dev ? out_ids : mids,
+                        dev ? out_scores : msc, mpos, g->device, st)))
+    return rc;
+  if ((rc = launch_gather_i64(arow, mpos, k_eff, 0, dev ? (out_rows ? out_rows : mrow) : mrow, st))) return rc;
+  if (dev) return OTF_OK;
+  if ((rc = g->h_out.ensure((size_t)k_eff * 32))) return rc;
+  OTF_CUDA(cudaMemcpyAsync(g->h_out.p, g->outbuf.p, (size_t)k_eff * 32, cudaMemcpyDeviceToHost, st));
+  OTF_CUDA(cudaStreamSynchronize(st));
+  const int64_t* h = static_cast<const int64_t*>(g->h_out.p);
+  std::memcpy(out_ids, h, (size_t)k_eff * 8);
+  std::memcpy(out_scores, h + k_eff, (size_t)k_eff * 8);
+  if (out_rows) std::memcpy(out_rows, h + 3 * k_eff, (size_t)k_eff * 8);
+  return OTF_OK;
+}

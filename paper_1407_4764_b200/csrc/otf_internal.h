@@ -85,6 +85,16 @@ int launch_batch_train(const void* X, int dt, int64_t n_pos, int64_t n, int d, c
 int launch_hinge_objective(const void* X, int dt, int64_t n_pos, int64_t n, int d, const double* w,
                            double lam, double* out, cudaStream_t st);
 
+// multi-GPU group (otf_group.cu)
+int group_unique_id(unsigned char* out128);
+int group_comm_create(int n_ranks, int rank, const unsigned char* id128, void** comm);
+void group_comm_destroy(void* comm);
+int group_broadcast_f64(void* comm, double* buf, int64_t n, int root, cudaStream_t st);
+int group_allgather_candidates(void* comm, const double* sc, const int64_t* ids, const int64_t* rows, int64_t k,
+                               double* sc_all, int64_t* ids_all, int64_t* rows_all, cudaStream_t st);
+int launch_group_finalize(double* sc, int64_t* ids, int64_t* rows, int64_t k_loc, int64_t k, int64_t row_offset,
+                          int64_t pad_base, cudaStream_t st);
+
 // misc
 int launch_gather_rows(const uint8_t* src, int64_t row_bytes, const int64_t* rows, int64_t n,
                        uint8_t* dst, int device, cudaStream_t st);

@@ -159,3 +159,76 @@ class ShardedRepository:
         sc, ids, rows = (self.backend.to_host(t) for t in out)
         names = tuple(self.names[int(r)] for r in rows) if self.names is not None else None
         return RankedList(ids.astype(np.int64), sc.astype(np.float64), ver, produced_at, names)
+
+
+class NcclShardGroup:
+    """The same collective ranking through the library's own NCCL communicator (otf_group_*).
+
+    One object per rank over that rank's shard. The 128-byte NCCL unique id is created once
+    (``NcclShardGroup.unique_id()`` on one rank) and handed to every rank by any channel (e.g.
+    ``torch.distributed.broadcast_object_list``). ``rank`` is collective; w is read on ``root``
+    only; every rank receives the global RankedList.
+    """
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _lib.check(_lib.load().otf_group_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, shard: Repository, uid: bytes, n_ranks: int, rank: int, row_offset: int, total_rows: int,
+                 names=None, root: int = 0):
+        if len(uid) != 128:
+            raise ConfigError("an NCCL unique id is 128 bytes")
+        self.shard = shard
+        self.row_offset = int(row_offset)
+        self.total_rows = int(total_rows)
+        self.names = names
+        self.root = int(root)
+        self.model_dim = shard.model_dim
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _lib.check(_lib.load().otf_group_create(shard.device, int(n_ranks), int(rank), buf, C.byref(h)))
+        self._handle = h
+
+    def close(self) -> None:
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.otf_group_destroy(h)
+        self._handle = None
+
+    def __del__(self):
+        self.close()
+
+    def rank(self, model, k: int, produced_at: float = 0.0) -> RankedList:
+        w = np.ascontiguousarray(as_weights(model), dtype=np.float64)
+        if w.shape != (self.model_dim,):
+            raise ConfigError(f"store dim {self.model_dim} does not match model dim {w.shape[0]}")
+        k_eff = max(0, min(int(k), self.total_rows))
+        ids = np.empty(k_eff, np.int64)
+        sc = np.empty(k_eff, np.float64)
+        rows = np.empty(k_eff, np.int64)
+        got = C.c_int64()
+        _lib.check(_lib.load().otf_group_rank(self._handle, self.shard.handle, _lib.ptr(w), self.root, self.row_offset,
+                                              self.total_rows, int(k), _lib.ptr(ids), _lib.ptr(sc), _lib.ptr(rows),
+                                              C.byref(got), _lib.MEM_HOST, None))
+        names = tuple(self.names[int(r)] for r in rows) if self.names is not None else None
+        return RankedList(ids, sc, model_version(model), produced_at, names)
+
+    def rank_device(self, w_dev, k: int, stream=None):
+        """Device tensors in and out (torch): returns (scores, ids, global rows) on this GPU."""
+        import torch
+
+        k_eff = max(0, min(int(k), self.total_rows))
+        dev = w_dev.device
+        sc = torch.empty(k_eff, dtype=torch.float64, device=dev)
+        ids = torch.empty(k_eff, dtype=torch.int64, device=dev)
+        rows = torch.empty(k_eff, dtype=torch.int64, device=dev)
+        if k_eff:
+            st = stream if stream is not None else torch.cuda.current_stream(dev)
+            got = C.c_int64()
+            _lib.check(_lib.load().otf_group_rank(self._handle, self.shard.handle, _lib.tptr(w_dev), self.root,
+                                                  self.row_offset, self.total_rows, int(k), _lib.tptr(ids),
+                                                  _lib.tptr(sc), _lib.tptr(rows), C.byref(got), _lib.MEM_DEVICE,
+                                                  C.c_void_p(st.cuda_stream)))
+        return sc, ids, rows
