@@ -47,6 +47,9 @@ CONFIGS = {
                         "Pegasos training concurrent with ranking (rank 0, own stream)"),
     "c3": dict(kind="pq", rows=10_000_000, dim=16, k=1000, subdim=8,
                workload="C3: 10M PQ codes per GPU (16 sub-quantizers x 256 centroids, 128-D), LUT score + top-1000"),
+    "c3e": dict(kind="pqenc", rows=10_000_000, dim=16, subdim=8, k=0,
+                workload="C3 ingest (SURVEY.md §8f): pq_encode of 10M x 128-D fp32 vectors per GPU "
+                         "under a 16 x 256 x 8 codebook (nearest centroid per block, float64)"),
     "c5a": dict(kind="binary", rows=100_000_000, dim=2048, k=1000,
                 workload="C5a: 100M x 2048-bit packed binary codes per GPU, score + top-1000"),
     "c5b": dict(kind="multi", rows=10_000_000, dim=4096, k=1000, n_cls=64,
@@ -69,6 +72,14 @@ def row_bytes(cfg) -> int:
     if cfg["kind"] == "pq":
         return cfg["dim"]
     return cfg["dim"] // 8
+
+
+def metric_unit(cfg) -> tuple[str, str]:
+    if cfg["kind"] == "pqenc":
+        return "vectors PQ-encoded/sec", "vectors/s"
+    if cfg["kind"] == "multi":
+        return "dataset images scored+ranked/sec", "image-classifier pairs/s"
+    return "dataset images scored+ranked/sec", "images/s"
 
 
 class ClockSampler:
@@ -145,6 +156,13 @@ def cpu_sample(cfg, seed=1234):
         w = rng.standard_normal(dim)
         fn = lambda: O.top_k(O.score_dense(w, x), k)
         desc = f"{rows} x {dim}-D fp32 rows (score_dense + top_k, ranker.py:63-143)"
+    elif kind == "pqenc":
+        rows = min(cfg["rows"], 40_000)
+        cents = rng.standard_normal((dim, 256, cfg["subdim"])).astype(np.float32)
+        x = rng.standard_normal((rows, dim * cfg["subdim"]), dtype=np.float32)
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        fn = lambda: O.pq_encode(cents, x)
+        desc = f"pq_encode of {rows} x {dim * cfg['subdim']}-D fp32 vectors, {dim} x 256 x {cfg['subdim']} codebook (pq.py:206-230)"
     elif kind == "pq":
         rows = min(cfg["rows"], 2_000_000)
         cents = rng.standard_normal((dim, 256, cfg["subdim"])).astype(np.float32)
@@ -190,14 +208,15 @@ def run_reference(args, cfg):
             break
     per = float(np.mean(times))
     value = rows / per
+    metric, unit = metric_unit(cfg)
     line = {
-        "impl": "reference", "metric": "dataset images scored+ranked/sec", "value": value, "unit": "images/s",
+        "impl": "reference", "metric": metric, "value": value, "unit": unit,
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["kind"] != "pq" else "f64",
         "data": "synthetic", "config": {"workload": cfg["workload"], "k": cfg["k"], "sample_rows": rows},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cpu_threads(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cpu_threads(), "kind": "port",
                          "sample": desc + " on host cores; the reference itself (pure numpy) cannot travel to the GPU box"},
-        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -517,6 +536,124 @@ def run_gpu(args, cfg):
     return 0
 
 
+# FFMA peak derived from the hardware (no FP32 SIMT peak in MEASURED_PEAKS.json):
+# 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def run_encode(args, cfg):
+    """C3 ingest: pq_encode of the whole batch of device-resident vectors per step (one GPU per
+    rank, each encodes its own rows). The kernel is FP32-FMA bound (K*Q fused multiply-adds per
+    vector and block, float32 screening with a float64 decision), so its roofline is FFMA
+    throughput, not HBM."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1407_4764_b200 as otf
+    from paper_1407_4764_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    otf.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, M, Q, K = cfg["rows"], cfg["dim"], cfg["subdim"], 256
+    dim = M * Q
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242 + rank)
+    x = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    for s0 in range(0, n, 1 << 21):
+        v = x[s0:s0 + (1 << 21)]
+        v.normal_(generator=g)
+        v /= v.norm(dim=1, keepdim=True)
+    cents_np = np.random.default_rng(99).standard_normal((M, K, Q)).astype(np.float32)
+    cents = torch.as_tensor(cents_np, device=dev)
+    codes = torch.empty((n, M), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    lib = _lib.load()
+
+    def step():
+        _lib.check(lib.otf_pq_encode(local, _lib.tptr(x), n, dim, _lib.tptr(cents), M, K, Q, _lib.tptr(codes),
+                                     _lib.MEM_DEVICE, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    steps = min(args.steps, 20)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    launches0 = _lib.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - launches0
+    ms = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n * world / (ms / 1e3)
+    flops = 2.0 * n * M * K * Q
+    achieved = flops / (ms / 1e3) / 1e12
+
+    # e2e through the public API: host vectors in, host codes out (a 1M-row batch per call)
+    e2e_rows = min(n, 1_000_000)
+    xh = x[:e2e_rows].cpu().numpy()
+    book = otf.PQCodebook(cents_np)
+    otf.pq_encode(book, xh[:1000])
+    e2e_t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        otf.pq_encode(book, xh)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_t))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rows_c, fn, desc = cpu_sample(cfg)
+        fn()
+        t0 = time.perf_counter()
+        fn()
+        cpu = {"value": rows_c / (time.perf_counter() - t0), "unit": "vectors/s", "cores": cpu_threads(),
+               "kind": "port", "sample": desc + ", oracle port (numpy, the reference's arithmetic), one run"}
+    if rank == 0:
+        metric, unit = metric_unit(cfg)
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 screening, f64 decision", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "rows_per_gpu": n, "dim": dim, "blocks": M,
+                       "centroids": K, "subdim": Q, "l2": "inputs (%.1f GB/GPU) larger than L2" % (n * dim * 4 / 1e9)},
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                         "kernel": "pq_encode_kernel<8>: 2*K*Q flop per vector and block (FFMA screening)",
+                         "hbm_gbs": n * (dim * 4 + M) / (ms / 1e3) / 1e9,
+                         "peak_source": "derived: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (no measured FP32 peak)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_rows / e2e_s, "unit": unit, "h2d_bytes_per_step": e2e_rows * dim * 4,
+                    "d2h_bytes_per_step": e2e_rows * M, "rows_per_call": e2e_rows},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,6 +677,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg["kind"] == "pqenc":
+        return run_encode(args, cfg)
     return run_gpu(args, cfg)
 
 

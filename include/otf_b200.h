@@ -145,6 +145,13 @@ int otf_unpack_bits(int device, const uint8_t* codes, int64_t n, int32_t output_
 int otf_binarize(int device, const double* frame, const float* centering, int32_t input_dim,
                  int32_t output_bits, const double* X, int64_t n, uint8_t* out, int mem,
                  void* stream);
+/* pq_encode(codebook, vectors) — pq.py:206-230 (ingest): vectors (n, dim) float32, centroids
+ * (num_blocks, num_centroids, subdim) float32 -> codes (n, num_blocks) uint8, nearest centroid
+ * per block in float64 (argmin_j |c_j|^2 - 2 x.c_j, first minimum). dim != num_blocks*subdim ->
+ * OTF_ERR_CONFIG (pq.py:218-219). */
+int otf_pq_encode(int device, const float* vectors, int64_t n, int32_t dim, const float* centroids,
+                  int32_t num_blocks, int32_t num_centroids, int32_t subdim, uint8_t* out_codes, int mem,
+                  void* stream);
 /* hamming_distance(a, b) — binary.py:123-128 (row-wise, equal widths). */
 int otf_hamming(int device, const uint8_t* a, const uint8_t* b, int64_t n, int32_t width,
                 int64_t* out, int mem, void* stream);

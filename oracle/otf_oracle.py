@@ -131,6 +131,29 @@ def lut_entry_numpy_order(c, w) -> float:
     return 0.0 + (acc0 + acc1)
 
 
+def pq_encode(centroids, vectors, chunk_rows: int = 1 << 18):
+    """pq.py:206-230 — nearest centroid per sub-block in float64: argmin_j (|c_j|^2 - 2 x.c_j)
+    (|x|^2 dropped), ties to the lowest index. Also returns the best and second-best distance
+    of every (row, block), so a test can tell a genuine near-tie (|d1 - d2| at rounding level,
+    where the BLAS dot order may pick either) from a real mismatch."""
+    cents64 = np.asarray(centroids, dtype=np.float32).astype(np.float64)
+    M, K, Q = cents64.shape
+    arr = np.asarray(vectors, dtype=np.float32)
+    norms = np.sum(cents64 * cents64, axis=2)
+    n = arr.shape[0]
+    codes = np.empty((n, M), dtype=np.uint8)
+    gap = np.empty((n, M), dtype=np.float64)
+    for start in range(0, n, chunk_rows):
+        chunk = arr[start:start + chunk_rows].astype(np.float64)
+        for m in range(M):
+            sq = norms[m][np.newaxis, :] - 2.0 * (chunk[:, m * Q:(m + 1) * Q] @ cents64[m].T)
+            a = np.argmin(sq, axis=1)
+            codes[start:start + len(chunk), m] = a.astype(np.uint8)
+            part = np.partition(sq, 1, axis=1) if K > 1 else np.concatenate([sq, sq + np.inf], axis=1)
+            gap[start:start + len(chunk), m] = part[:, 1] - part[:, 0]
+    return codes, gap
+
+
 def pairwise_sum_numpy_order(a) -> float:
     """numpy's pairwise summation of a contiguous float64 run (add.reduce inner loop)."""
     n = len(a)

@@ -655,6 +655,14 @@ struct Scratch {
     *dptr = bufs.back().p;
     return OTF_OK;
   }
+  // device scratch in either mode (released, after the work completes, by cudaFree)
+  int tmp(size_t bytes, void** dptr) {
+    bufs.emplace_back();
+    int rc = bufs.back().ensure(bytes > 0 ? bytes : 16);
+    if (rc) return rc;
+    *dptr = bufs.back().p;
+    return OTF_OK;
+  }
   int out(void* user, const void* dptr, size_t bytes, int mem) {
     if (mem == OTF_MEM_DEVICE) return OTF_OK;
     if (bytes) OTF_CUDA(cudaMemcpyAsync(user, dptr, bytes, cudaMemcpyDeviceToHost, st));
@@ -770,6 +778,30 @@ int otf_binarize(int device, const double* frame, const float* centering, int32_
                             output_bits, static_cast<const double*>(dX), n, static_cast<uint8_t*>(dout),
                             device, st))) return rc;
   return S.out(out, dout, (size_t)n * row_bytes, mem);
+}
+
+int otf_pq_encode(int device, const float* vectors, int64_t n, int32_t dim, const float* centroids,
+                  int32_t num_blocks, int32_t num_centroids, int32_t subdim, uint8_t* out_codes, int mem,
+                  void* stream) {
+  if (num_blocks <= 0 || num_centroids <= 0 || subdim <= 0) return fail(OTF_ERR_CONFIG, "bad codebook shape");
+  if (num_centroids > 256) return fail(OTF_ERR_CONFIG, "num_centroids must fit a byte (<= 256)");
+  if ((int64_t)dim != (int64_t)num_blocks * subdim)
+    return fail(OTF_ERR_CONFIG, "vector dim " + std::to_string(dim) + " does not match codebook dim " +
+                                    std::to_string((int64_t)num_blocks * subdim));
+  if (n < 0) return fail(OTF_ERR_CONFIG, "n must be >= 0");
+  if (n == 0) return OTF_OK;
+  STATELESS_BEGIN(device, mem, stream)
+  const void *dX, *dc;
+  void *dout, *dnorm;
+  const size_t cb = (size_t)num_blocks * num_centroids * subdim * 4;
+  if ((rc = S.in(vectors, (size_t)n * dim * 4, mem, &dX))) return rc;
+  if ((rc = S.in(centroids, cb, mem, &dc))) return rc;
+  if ((rc = S.outbuf(out_codes, (size_t)n * num_blocks, mem, &dout))) return rc;
+  if ((rc = S.tmp(pq_encode_scratch_bytes(num_blocks, num_centroids), &dnorm))) return rc;
+  if ((rc = launch_pq_encode(static_cast<const float*>(dX), n, num_blocks, num_centroids, subdim,
+                             static_cast<const float*>(dc), dnorm, static_cast<uint8_t*>(dout), device, st)))
+    return rc;
+  return S.out(out_codes, dout, (size_t)n * num_blocks, mem);
 }
 
 int otf_hamming(int device, const uint8_t* a, const uint8_t* b, int64_t n, int32_t width,

@@ -15,6 +15,10 @@ int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, fl
 // pq (otf_pq.cu)
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
                   cudaStream_t st);
+// pq_encode (pq.py:206-230): X (n, M*Q) f32, cents (M,K,Q) f32 -> codes (n, M) u8.
+size_t pq_encode_scratch_bytes(int M, int K);
+int launch_pq_encode(const float* X, int64_t n, int M, int K, int Q, const float* cents, void* scratch,
+                     uint8_t* codes, int device, cudaStream_t st);
 int launch_pq_check(const uint8_t* codes, int64_t total, int K, unsigned int* bad, int device,
                     cudaStream_t st);
 bool pq_fast_path(int M, const uint8_t* codes);

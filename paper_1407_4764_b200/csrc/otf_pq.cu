@@ -16,6 +16,8 @@
 //
 // HBM roofline: M bytes per row (16 B for C3). The LUT (M*256*8 B) lives in shared memory;
 // the scan is shared-memory-lookup bound for M=16.
+#include <algorithm>
+
 #include "otf_common.cuh"
 #include "otf_internal.h"
 
@@ -393,6 +395,219 @@ int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, c
   pq_scan_generic<<<(int)grid, 256, 0, st>>>(codes, n, M, lut, K, out, hist);
   OTF_LAUNCH_CHECK("pq_scan_generic");
   return OTF_OK;
+}
+
+// ---- pq_encode (pq.py:206-230): the ingest path of PQ repositories ----------------------------
+// code[i, m] = argmin_j (|c_mj|^2 - 2 x_im . c_mj) in float64 (|x|^2 is dropped, as the reference
+// does), ties and NaNs resolved like numpy's argmin (first minimum / first NaN). |c|^2 follows
+// numpy's pairwise order (np.sum, pq.py:222) and 2.0*dot is exact, so the only arithmetic that
+// can differ from the reference is the Q-term dot (OpenBLAS dgemm order, not pinnable): codes
+// agree except at genuine rounding-level near-ties (tests accept a differing code only where
+// the two float64 distances differ by < 1e-12 relative).
+//
+// Float32 screening, float64 decision: every distance is first computed in float32 (FFMA, twice
+// the float64 rate and no float32->float64 conversions), tracking the best and second-best. The
+// float32 error of a distance is below eps = 2^-20 (max_j |c_j|^2 + 2 |x| max_j |c_j|) (a 4x
+// margin over the FFMA-chain bound), so when the runner-up is more than 2 eps behind, the
+// float32 winner is the float64 argmin. Otherwise (near-ties, duplicate centroids, NaN/Inf
+// anywhere) the (row, block) is decided by the exact float64 loop with numpy's semantics.
+// One thread per row; a CTA keeps the float32 centroids, both norms and per-block bounds of a
+// group of G sub-quantizers in shared memory (all lanes read the same centroid: broadcast).
+__global__ void pq_cent_norms_kernel(const float* __restrict__ cents, int MK, int Q, double* __restrict__ norms) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < MK; t += gridDim.x * blockDim.x) {
+    const float* c = cents + (int64_t)t * Q;
+    auto sq = [c](int i) { const double v = (double)c[i]; return __dmul_rn(v, v); };
+    norms[t] = pairwise_sum(sq, 0, Q);
+  }
+}
+
+// per block m: [max_j |c_j|^2, max_j |c_j|, 1 if any centroid or norm is not finite]
+__global__ void pq_block_bounds_kernel(const float* __restrict__ cents, const double* __restrict__ norms, int M,
+                                       int K, int Q, float* __restrict__ bounds) {
+  const int m = blockIdx.x;
+  __shared__ float s_n[32], s_c[32];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  float nmax = 0.f, cmax = 0.f;
+  int bad = 0;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const double nj = norms[(int64_t)m * K + j];
+    if (!isfinite(nj)) bad = 1;
+    nmax = fmaxf(nmax, (float)nj);
+    cmax = fmaxf(cmax, (float)sqrt(nj));
+  }
+  for (int o = 16; o; o >>= 1) {
+    nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  }
+  if (bad) atomicOr(&s_bad, 1);
+  if ((threadIdx.x & 31) == 0) { s_n[threadIdx.x >> 5] = nmax; s_c[threadIdx.x >> 5] = cmax; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { nmax = fmaxf(nmax, s_n[w]); cmax = fmaxf(cmax, s_c[w]); }
+    bounds[3 * m] = nmax;
+    bounds[3 * m + 1] = cmax;
+    bounds[3 * m + 2] = s_bad ? 1.f : 0.f;
+  }
+}
+
+__device__ int encode_exact(const float* __restrict__ xs, const float* __restrict__ cg, const double* __restrict__ ng,
+                            int K, int Q) {
+  double best = 0.0;
+  int arg = 0;
+  bool nan_seen = false;
+  for (int j = 0; j < K; ++j) {
+    const float* c = cg + (size_t)j * Q;
+    double dot = 0.0;
+    for (int q = 0; q < Q; ++q) dot = __fma_rn((double)__ldg(xs + q), (double)c[q], dot);
+    const double sq = __dsub_rn(ng[j], 2.0 * dot);
+    if (j == 0) {
+      best = sq;
+      nan_seen = isnan(sq);
+    } else if (!nan_seen) {
+      if (isnan(sq)) { arg = j; nan_seen = true; }
+      else if (sq < best) { best = sq; arg = j; }
+    }
+  }
+  return arg;
+}
+
+template <int QR>  // QR > 0: Q == QR, float32 screening in registers; QR == 0: any Q, exact path only
+__global__ void __launch_bounds__(256) pq_encode_kernel(const float* __restrict__ X, int64_t n, int dim,
+                                                        const float* __restrict__ cents,
+                                                        const double* __restrict__ norms,
+                                                        const float* __restrict__ bounds, int M, int K, int Q,
+                                                        int G, uint8_t* __restrict__ codes) {
+  // Two rows per thread and centroids read as float4 (broadcast) so a warp issues ~1 shared
+  // load per 7 FFMAs (scalar loads made the first version LSU-bound at 9 loads per 8 FFMAs).
+  constexpr int RPT = 2;
+  extern __shared__ __align__(16) unsigned char enc_smem[];
+  const int m0 = blockIdx.y * G;
+  const int g_n = min(G, M - m0);
+  const int Kp = (K + 3) & ~3;                                   // padded to whole float4s
+  double* sn = reinterpret_cast<double*>(enc_smem);            // [g][Kp] float64 norms
+  float* sn32 = reinterpret_cast<float*>(sn + (size_t)G * Kp);  // [g][Kp] float32 norms (+inf pad)
+  float* sb = sn32 + (size_t)G * Kp;                            // [g][4] bounds
+  float* sc = sb + 4 * G;                                       // [g][Kp][Q] centroids (16-B aligned)
+  for (int t = threadIdx.x; t < g_n * Kp; t += blockDim.x) {
+    const int g = t / Kp, j = t % Kp;
+    const double v = j < K ? norms[(int64_t)(m0 + g) * K + j] : 0.0;
+    sn[t] = v;
+    sn32[t] = j < K ? (float)v : __int_as_float(0x7f800000);
+  }
+  for (int t = threadIdx.x; t < 3 * g_n; t += blockDim.x) sb[(t / 3) * 4 + t % 3] = bounds[3 * m0 + t];
+  for (int t = threadIdx.x; t < g_n * Kp * Q; t += blockDim.x) {
+    const int g = t / (Kp * Q), r = t % (Kp * Q);
+    sc[t] = r < K * Q ? cents[((int64_t)(m0 + g) * K) * Q + r] : 0.f;
+  }
+  __syncthreads();
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RPT; r0 < n; r0 += nthreads * RPT) {
+    for (int g = 0; g < g_n; ++g) {
+      const int m = m0 + g;
+      const float* cg = sc + (size_t)g * Kp * Q;
+      int code[RPT];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) code[u] = -1;
+      if constexpr (QR > 0) {
+        static_assert(QR % 4 == 0, "float4 centroid loads");
+        float x[RPT][QR], xx[RPT], d1[RPT], d2[RPT];
+        int a1[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int64_t row = r0 + u < n ? r0 + u : n - 1;
+          const float* xs = X + row * dim + (int64_t)m * QR;
+          xx[u] = 0.f;
+#pragma unroll
+          for (int q = 0; q < QR; ++q) { x[u][q] = __ldg(xs + q); xx[u] = fmaf(x[u][q], x[u][q], xx[u]); }
+          d1[u] = d2[u] = __int_as_float(0x7f800000);
+          a1[u] = 0;
+        }
+        const float4* n4 = reinterpret_cast<const float4*>(sn32 + (size_t)g * Kp);
+        for (int j0 = 0; j0 < Kp; j0 += 4) {
+          const float4 nn = n4[j0 >> 2];
+          const float nj[4] = {nn.x, nn.y, nn.z, nn.w};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const float4* c4 = reinterpret_cast<const float4*>(cg + (size_t)(j0 + jj) * QR);
+            float c[QR];
+#pragma unroll
+            for (int v = 0; v < QR / 4; ++v) {
+              const float4 t4 = c4[v];
+              c[4 * v] = t4.x; c[4 * v + 1] = t4.y; c[4 * v + 2] = t4.z; c[4 * v + 3] = t4.w;
+            }
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+              float dot = 0.f;
+#pragma unroll
+              for (int q = 0; q < QR; ++q) dot = fmaf(x[u][q], c[q], dot);
+              const float d = fmaf(-2.f, dot, nj[jj]);
+              const bool lt = d < d1[u];
+              d2[u] = lt ? d1[u] : fminf(d2[u], d);
+              a1[u] = lt ? j0 + jj : a1[u];
+              d1[u] = lt ? d : d1[u];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const float eps = 0x1p-20f * (sb[4 * g] + 2.f * sqrtf(xx[u]) * sb[4 * g + 1]);
+          if (sb[4 * g + 2] == 0.f && d2[u] - d1[u] > 2.f * eps) code[u] = a1[u];  // NaN fails this test
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t row = r0 + u;
+        if (row >= n) continue;
+        if (code[u] < 0) code[u] = encode_exact(X + row * dim + (int64_t)m * Q, cg, sn + (size_t)g * Kp, K, Q);
+        codes[row * M + m] = (uint8_t)code[u];
+      }
+    }
+  }
+}
+
+// vectors (n, M*Q) float32, centroids (M, K, Q) float32 on the device -> codes (n, M) uint8.
+// scratch: M*K float64 norms + 3*M float32 bounds (pq_encode_scratch_bytes).
+size_t pq_encode_scratch_bytes(int M, int K) { return (size_t)M * K * 8 + (size_t)M * 3 * 4 + 16; }
+
+int launch_pq_encode(const float* X, int64_t n, int M, int K, int Q, const float* cents, void* scratch,
+                     uint8_t* codes, int device, cudaStream_t st) {
+  if (n <= 0) return OTF_OK;
+  if (K < 1 || K > 256) return fail(OTF_ERR_CONFIG, "num_centroids must be in 1..256");
+  double* norms = static_cast<double*>(scratch);
+  float* bounds = reinterpret_cast<float*>(norms + (size_t)M * K);
+  const int MK = M * K;
+  pq_cent_norms_kernel<<<(MK + 255) / 256, 256, 0, st>>>(cents, MK, Q, norms);
+  OTF_LAUNCH_CHECK("pq_cent_norms_kernel");
+  pq_block_bounds_kernel<<<M, 256, 0, st>>>(cents, norms, M, K, Q, bounds);
+  OTF_LAUNCH_CHECK("pq_block_bounds_kernel");
+  const size_t Kp = (size_t)((K + 3) & ~3);
+  const size_t per_m = Kp * Q * 4 + Kp * 12 + 16;
+  const size_t budget = 200 * 1024;
+  if (per_m > budget) return fail(OTF_ERR_CONFIG, "sub-quantizer too large for pq_encode (K*Q*4 > 200 KB)");
+  const int G = (int)std::min<size_t>((size_t)M, budget / per_m);
+  const size_t smem = per_m * G;
+  const int groups = (M + G - 1) / G;
+  const int dim = M * Q;
+  auto launch = [&](auto fn) -> int {
+    OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t bx = (int64_t)per_sm * sm_count(device);
+    const int64_t need = (n + 511) / 512;  // two rows per thread
+    if (need < bx) bx = need;
+    fn<<<dim3((unsigned)bx, (unsigned)groups), 256, smem, st>>>(X, n, dim, cents, norms, bounds, M, K, Q, G, codes);
+    OTF_LAUNCH_CHECK("pq_encode_kernel");
+    return OTF_OK;
+  };
+  switch (Q) {
+    case 4: return launch(pq_encode_kernel<4>);
+    case 8: return launch(pq_encode_kernel<8>);
+    case 16: return launch(pq_encode_kernel<16>);
+    default: return launch(pq_encode_kernel<0>);
+  }
 }
 
 }  // namespace otf

@@ -2,8 +2,9 @@
 
 ``build_score_lut`` and ``score_codes`` keep the reference's signatures and return the
 reference's float64 values bit-for-bit: the CUDA kernels (csrc/otf_pq.cu) replay numpy's
-einsum and pairwise-sum orders. Codebook learning, encoding and the OTFQ/OTFC formats are
-offline and out of scope; ``PQCodebook`` here is the container only, and any
+einsum and pairwise-sum orders. ``pq_encode`` (pq.py:206-230, the ingest path of a PQ
+repository) runs on the GPU too. Codebook learning and the OTFQ/OTFC formats
+are offline and out of scope; ``PQCodebook`` here is the container only, and any
 object with ``centroids`` / ``num_blocks`` / ``num_centroids`` / ``subdim`` works (e.g. the
 reference's own PQCodebook).
 """
@@ -96,4 +97,29 @@ def score_codes(lut, codes, chunk_rows: int = 1 << 18) -> np.ndarray:
     out = np.empty(arr.shape[0], dtype=np.float64)
     _lib.check(lib.otf_pq_score_codes(_lib.default_device(), _lib.ptr(table), m, k, _lib.ptr(arr),
                                       arr.shape[0], _lib.ptr(out), _lib.MEM_HOST, None))
+    return out[0] if single else out
+
+
+def pq_encode(codebook, vectors, chunk_rows: int = 1 << 18) -> np.ndarray:
+    """pq.py:206-230 — (n, num_blocks) uint8 codes, nearest centroid per block in float64.
+
+    A single (dim,) vector gives a (num_blocks,) code. ``chunk_rows`` is accepted for signature
+    parity (the GPU encodes all rows in one launch). The distance |c|^2 - 2 x.c is the
+    reference's; only its Q-term dot may round differently from OpenBLAS's, so a code can differ
+    only where two centroids are equidistant to rounding level.
+    """
+    del chunk_rows
+    cents = _centroids(codebook)
+    m, k, q = cents.shape
+    arr = np.asarray(vectors, dtype=np.float32)
+    single = arr.ndim == 1
+    if single:
+        arr = arr[np.newaxis, :]
+    arr = np.ascontiguousarray(arr)
+    if arr.shape[1] != m * q:
+        raise ConfigError(f"vector dim {arr.shape[1]} does not match codebook dim {m * q}")
+    out = np.empty((arr.shape[0], m), dtype=np.uint8)
+    if arr.shape[0]:
+        _lib.check(_lib.load().otf_pq_encode(_lib.default_device(), _lib.ptr(arr), arr.shape[0], arr.shape[1],
+                                             _lib.ptr(cents), m, k, q, _lib.ptr(out), _lib.MEM_HOST, None))
     return out[0] if single else out

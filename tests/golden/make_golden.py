@@ -68,6 +68,18 @@ def main() -> None:
         g[f"pq_{name}_rank_ids"] = ranked.ids
         g[f"pq_{name}_rank_scores"] = ranked.scores
 
+    # ---- pq_encode (pq.py:206-230): codes of fresh vectors under a learned codebook ------------
+    for name, (m, k, q, n_train, n, seed) in {"e16": (16, 256, 8, 3000, 2000, 61),
+                                              "e4k16": (4, 16, 5, 400, 700, 62)}.items():
+        rng = np.random.default_rng(seed)
+        train = normalize_rows(rng.standard_normal((n_train, m * q))).astype(np.float32)
+        book = rpq.learn_pq_codebook(train, rpq.PQConfig(subdim=q, num_centroids=k, iterations=6, seed=seed))
+        vecs = normalize_rows(rng.standard_normal((n, m * q))).astype(np.float32)
+        vecs[:5] = book.centroids[:, :5, :].transpose(1, 0, 2).reshape(5, m * q)  # exact centroid hits
+        g[f"pqenc_{name}_cents"] = book.centroids
+        g[f"pqenc_{name}_vecs"] = vecs
+        g[f"pqenc_{name}_codes"] = rpq.pq_encode(book, vecs)
+
     # ---- binary (ranker.py:78-94, binary.py:86-128) ----------------------------------------
     for name, (m, bits, n, seed) in {"b32": (8, 32, 200, 21), "b2048": (128, 2048, 300, 22),
                                      "b19": (8, 19, 150, 23), "b1024": (64, 1024, 300, 24)}.items():

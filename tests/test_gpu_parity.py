@@ -408,3 +408,48 @@ def test_train_batch_reference_behaviour(otf):
         otf.train_batch(np.empty((0, 4)), np.ones((3, 4)))
     with pytest.raises(otf.ConfigError):
         otf.BatchTrainConfig(c=0.0).validate()
+
+
+# ---- pq_encode (pq.py:206-230), the PQ ingest path ----------------------------------------------
+def _codes_agree(gpu, ref, gap, cents, vecs):
+    """Codes equal the reference's except at genuine near-ties: where they differ, the two
+    centroids' float64 distances must agree to rounding level (BLAS dot order)."""
+    bad = np.argwhere(gpu != ref)
+    for i, m in bad:
+        q = cents.shape[2]
+        x = vecs[i, m * q:(m + 1) * q].astype(np.float64)
+        c = cents[m].astype(np.float64)
+        d = (c * c).sum(1) - 2.0 * (c @ x)
+        a, b = d[int(gpu[i, m])], d[int(ref[i, m])]
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(a), abs(b)), (i, m, a, b)
+    return len(bad)
+
+
+@pytest.mark.parametrize("name", ["e16", "e4k16"])
+def test_pq_encode_matches_reference_golden(otf, golden, name):
+    cents, vecs = golden[f"pqenc_{name}_cents"], golden[f"pqenc_{name}_vecs"]
+    book = otf.PQCodebook(cents)
+    codes = otf.pq_encode(book, vecs)
+    assert codes.dtype == np.uint8 and codes.shape == golden[f"pqenc_{name}_codes"].shape
+    np.testing.assert_array_equal(codes, golden[f"pqenc_{name}_codes"])
+    np.testing.assert_array_equal(otf.pq_encode(book, vecs[3]), golden[f"pqenc_{name}_codes"][3])  # single
+
+
+@pytest.mark.parametrize("m,k,q,n", [(16, 256, 8, 20_000), (8, 256, 16, 5000), (3, 100, 7, 3000),
+                                     (2, 256, 40, 1000), (32, 256, 4, 4000)])
+def test_pq_encode_matches_oracle(otf, m, k, q, n):
+    rng = np.random.default_rng(m * 1000 + q)
+    cents = rng.standard_normal((m, k, q)).astype(np.float32)
+    cents[:, 1] = cents[:, 0]  # duplicate centroid: exact tie -> lowest index
+    vecs = rng.standard_normal((n, m * q)).astype(np.float32)
+    ref, gap = O.pq_encode(cents, vecs)
+    gpu = otf.pq_encode(otf.PQCodebook(cents), vecs)
+    assert _codes_agree(gpu, ref, gap, cents, vecs) <= max(1, n * m // 100_000)
+    assert not np.any(gpu == 1)  # the duplicate of centroid 0 is never chosen
+
+
+def test_pq_encode_errors_and_empty(otf):
+    book = otf.PQCodebook(np.zeros((2, 4, 3), np.float32))
+    with pytest.raises(otf.ConfigError):
+        otf.pq_encode(book, np.zeros((5, 7), np.float32))
+    assert otf.pq_encode(book, np.zeros((0, 6), np.float32)).shape == (0, 2)

@@ -140,3 +140,10 @@ def test_train_batch_matches_reference(golden, name, epochs, seed):
     np.testing.assert_array_equal(w, golden[f"tb_{name}_w"])
     assert total == int(golden[f"tb_{name}_iter"][0])
     np.testing.assert_array_equal(np.array(hist), golden[f"tb_{name}_hist"])
+
+
+@pytest.mark.parametrize("name", ["e16", "e4k16"])
+def test_oracle_pq_encode_matches_reference(golden, name):
+    codes, gap = O.pq_encode(golden[f"pqenc_{name}_cents"], golden[f"pqenc_{name}_vecs"])
+    np.testing.assert_array_equal(codes, golden[f"pqenc_{name}_codes"])
+    assert np.all(gap >= 0)
