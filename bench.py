@@ -50,6 +50,9 @@ CONFIGS = {
     "c3e": dict(kind="pqenc", rows=10_000_000, dim=16, subdim=8, k=0,
                 workload="C3 ingest (SURVEY.md §8f): pq_encode of 10M x 128-D fp32 vectors per GPU "
                          "under a 16 x 256 x 8 codebook (nearest centroid per block, float64)"),
+    "c3k": dict(kind="pqlearn", rows=50_000, dim=16, subdim=8, k=256, iterations=8,
+                workload="C3 codebook (SURVEY.md §8f): learn_pq_codebook on 50k x 128-D fp32 training vectors, "
+                         "16 blocks x 256 centroids x 8 dims, 8 Lloyd iterations"),
     "c5a": dict(kind="binary", rows=100_000_000, dim=2048, k=1000,
                 workload="C5a: 100M x 2048-bit packed binary codes per GPU, score + top-1000"),
     "c5b": dict(kind="multi", rows=10_000_000, dim=4096, k=1000, n_cls=64,
@@ -75,6 +78,8 @@ def row_bytes(cfg) -> int:
 
 
 def metric_unit(cfg) -> tuple[str, str]:
+    if cfg["kind"] == "pqlearn":
+        return "PQ codebook learning time (learn_pq_codebook)", "ms"
     if cfg["kind"] == "pqenc":
         return "vectors PQ-encoded/sec", "vectors/s"
     if cfg["kind"] == "multi":
@@ -156,6 +161,15 @@ def cpu_sample(cfg, seed=1234):
         w = rng.standard_normal(dim)
         fn = lambda: O.top_k(O.score_dense(w, x), k)
         desc = f"{rows} x {dim}-D fp32 rows (score_dense + top_k, ranker.py:63-143)"
+    elif kind == "pqlearn":
+        x = rng.standard_normal((cfg["rows"], dim * cfg["subdim"]), dtype=np.float32)
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        blocks = 2  # of dim; the per-block work is identical, the value is scaled to all blocks
+        sub = x[:, :blocks * cfg["subdim"]]
+        fn = lambda: O.learn_pq_codebook(sub, cfg["subdim"], cfg["k"], cfg["iterations"], 5)
+        desc = (f"learn_pq_codebook on {cfg['rows']} x {blocks * cfg['subdim']}-D ({blocks} of {dim} blocks, "
+                f"{cfg['k']} centroids, {cfg['iterations']} iterations, pq.py:116-203); value scaled x{dim // blocks}")
+        return dim / blocks, fn, desc
     elif kind == "pqenc":
         rows = min(cfg["rows"], 40_000)
         cents = rng.standard_normal((dim, 256, cfg["subdim"])).astype(np.float32)
@@ -209,10 +223,13 @@ def run_reference(args, cfg):
     per = float(np.mean(times))
     value = rows / per
     metric, unit = metric_unit(cfg)
+    if cfg["kind"] == "pqlearn":  # time-like: ms for the whole codebook (rows = block scale factor)
+        value = per * rows * 1e3
     line = {
         "impl": "reference", "metric": metric, "value": value, "unit": unit,
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": per * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["kind"] != "pq" else "f64",
+        "higher_is_better": cfg["kind"] != "pqlearn", "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if cfg["kind"] not in ("pq", "pqlearn") else "f64",
         "data": "synthetic", "config": {"workload": cfg["workload"], "k": cfg["k"], "sample_rows": rows},
         "cpu_baseline": {"value": value, "unit": unit, "cores": cpu_threads(), "kind": "port",
                          "sample": desc + " on host cores; the reference itself (pure numpy) cannot travel to the GPU box"},
@@ -654,6 +671,69 @@ def run_encode(args, cfg):
     return 0
 
 
+def run_learn(args, cfg):
+    """C3 codebook: learn_pq_codebook through the public API (host training matrix in, host
+    codebook out — the call a user makes; every step's H2D/D2H is inside the timed region).
+    GPU launches: the Lloyd assignment / objective / mean kernels of every block and iteration."""
+    import torch
+
+    import paper_1407_4764_b200 as otf
+    from paper_1407_4764_b200 import _lib
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    otf.set_device(local)
+    rng = np.random.default_rng(1234)
+    x = rng.standard_normal((cfg["rows"], cfg["dim"] * cfg["subdim"]), dtype=np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    pcfg = otf.PQConfig(subdim=cfg["subdim"], num_centroids=cfg["k"], iterations=cfg["iterations"], seed=5)
+    for _ in range(args.warmup):
+        otf.learn_pq_codebook(x, pcfg)
+    steps = min(args.steps, 5)
+    launches0 = _lib.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            book = otf.learn_pq_codebook(x, pcfg)
+            times.append(time.perf_counter() - t0)
+    launches = _lib.launch_count() - launches0
+    ms = float(np.mean(times)) * 1e3
+    iters = sum(len(h) for h in book.objective_history)
+    n, K, Q = cfg["rows"], cfg["k"], cfg["subdim"]
+    flops = 2.0 * n * K * Q * iters  # the assignment's float64 FMAs
+    achieved = flops / (ms / 1e3) / 1e12
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        scale, fn, desc = cpu_sample(cfg)
+        t0 = time.perf_counter()
+        fn()
+        cpu = {"value": (time.perf_counter() - t0) * scale * 1e3, "unit": "ms", "cores": cpu_threads(), "kind": "port",
+               "sample": desc + ", oracle port (numpy), one run"}
+    if rank == 0:
+        metric, unit = metric_unit(cfg)
+        print(json.dumps({
+            "metric": metric, "value": ms, "unit": unit, "n_gpus": 1, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "rows": n, "blocks": cfg["dim"], "centroids": K, "subdim": Q,
+                       "lloyd_iterations_run": iters, "l2": "training set (25.6 MB) is L2-resident by design"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": 37.0, "unit": "TFLOP/s",
+                         "frac": achieved / 37.0, "traffic": None,
+                         "kernel": "km_assign (2*K*Q flop per training vector and iteration), whole call timed",
+                         "peak_source": "nominal B200 FP64 (NVIDIA spec); the call is latency-bound "
+                                        "(per-iteration host round trips), see DESIGN.md"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ms, "unit": unit, "h2d_bytes_per_step": n * cfg["dim"] * Q * 8,
+                    "d2h_bytes_per_step": iters * (n * 4 + K * 8 + K * Q * 8 + 8)},
+            "gpu_launches": launches // steps,
+            "clocks": clk.summary(),
+        }), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -679,6 +759,8 @@ def main():
         return run_reference(args, cfg)
     if cfg["kind"] == "pqenc":
         return run_encode(args, cfg)
+    if cfg["kind"] == "pqlearn":
+        return run_learn(args, cfg)
     return run_gpu(args, cfg)
 
 

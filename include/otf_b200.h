@@ -215,6 +215,20 @@ int otf_trainer_weights_ptr(otf_trainer* tr, const double** out);
 /* The trainer's CUDA stream (high priority; runs concurrently with ranking). */
 int otf_trainer_stream(otf_trainer* tr, void** out);
 
+/* ---- PQ codebook learning (learn_pq_codebook / _lloyd, pq.py:116-203) --------------------------
+ * A handle keeps one block's float64 training sub-vectors (n, dim) on the device. Each step is
+ * _assign (pq.py:100-113) + the plain mean update (pq.py:155-162): on return, assign (n) and
+ * counts (k) describe the assignment to the centroids passed in, *objective = sum of the clamped
+ * best distances (the history entry), and centroids (k*dim, in/out) hold the means of the
+ * clusters with members (others unchanged). The caller runs the convergence test and the
+ * empty-cluster re-seeding (pq.py:146-171) on these host copies. */
+typedef struct otf_kmeans otf_kmeans;
+int otf_kmeans_create(int device, const double* data, int64_t n, int32_t dim, int32_t k, otf_kmeans** out);
+/* Replace the training sub-vectors (same n and dim): the next block of learn_pq_codebook. */
+int otf_kmeans_load(otf_kmeans* h, const double* data);
+int otf_kmeans_destroy(otf_kmeans* h);
+int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* counts, double* objective);
+
 /* ---- multi-GPU group (one process per GPU, shards by image) ------------
  * A native NCCL communicator over the ranks' shard handles. NCCL is loaded at run time
  * (libnccl.so.2, the one torch already mapped if any), so the library itself has no link-time

@@ -154,6 +154,60 @@ def pq_encode(centroids, vectors, chunk_rows: int = 1 << 18):
     return codes, gap
 
 
+def lloyd(data, k: int, iterations: int, rng, init=None):
+    """pq.py:100-171 — Lloyd k-means on one sub-block in float64: squared distances
+    |x|^2 - 2 x.c + |c|^2, first-minimum assignment, objective = sum of clamped best distances
+    (recorded before the update), stop when an assignment repeats after a plain update, means of
+    non-empty clusters, each empty cluster re-seeded at the member of the (current) largest
+    cluster farthest from its mean. Initial centroids: k distinct unique rows via rng.choice."""
+    x = np.asarray(data, dtype=np.float64)
+    if init is None:
+        uniq = np.unique(x, axis=0)
+        if uniq.shape[0] < k:
+            raise ValueError("too few distinct rows")
+        cents = uniq[rng.choice(uniq.shape[0], size=k, replace=False)].copy()
+    else:
+        cents = np.asarray(init, dtype=np.float64).copy()
+    hist = []
+    prev, plain = None, True
+    for _ in range(iterations):
+        d2 = (x * x).sum(1)[:, None] - 2.0 * (x @ cents.T) + (cents * cents).sum(1)[None, :]
+        lab = d2.argmin(1)
+        hist.append(float(np.maximum(d2[np.arange(len(x)), lab], 0.0).sum()))
+        if prev is not None and plain and np.array_equal(lab, prev):
+            break
+        prev = lab
+        cnt = np.bincount(lab, minlength=k)
+        empty = np.flatnonzero(cnt == 0)
+        plain = empty.size == 0
+        for j in range(k):
+            if cnt[j]:
+                cents[j] = x[lab == j].mean(0)
+        for j in empty:
+            big = int(np.argmax(cnt))
+            mem = np.flatnonzero(lab == big)
+            far = mem[int(np.argmax(((x[mem] - cents[big]) ** 2).sum(1)))]
+            cents[j] = x[far]
+            lab[far] = j
+            cnt[big] -= 1
+            cnt[j] += 1
+    return cents, hist
+
+
+def learn_pq_codebook(train, subdim: int, k: int, iterations: int, seed: int):
+    """pq.py:174-203 — blocks in order, one rng; returns (float32 centroids, histories, centering)."""
+    data = np.asarray(train, dtype=np.float32)
+    rng = np.random.default_rng(seed)
+    blocks = data.shape[1] // subdim
+    out = np.empty((blocks, k, subdim), dtype=np.float32)
+    hists = []
+    for m in range(blocks):
+        c, h = lloyd(data[:, m * subdim:(m + 1) * subdim], k, iterations, rng)
+        out[m] = c.astype(np.float32)
+        hists.append(h)
+    return out, hists, data.astype(np.float64).mean(0).astype(np.float32)
+
+
 def pairwise_sum_numpy_order(a) -> float:
     """numpy's pairwise summation of a contiguous float64 run (add.reduce inner loop)."""
     n = len(a)

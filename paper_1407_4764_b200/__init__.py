@@ -22,7 +22,7 @@ from .errors import (
     RetrievalError,
 )
 from .model import LinearModel
-from .pq import PQCodebook, build_score_lut, pq_encode, score_codes
+from .pq import PQCodebook, PQConfig, build_score_lut, learn_pq_codebook, pq_encode, score_codes
 from .ranker import RankedList, RankerConfig, Repository, score_binary, score_dense, score_pq, top_k
 from .store import FeatureStore
 from .trainer import BatchTrainConfig, OnlineTrainer, TrainerConfig, hinge_objective, pegasos_step, train_batch
@@ -32,7 +32,7 @@ __all__ = [
     "BinaryCodec", "TightFrame", "binarize", "hamming_distance", "unpack_bits",
     "ConfigError", "CorruptionError", "DegenerateInputError", "EmptyStoreError", "FormatError",
     "InsufficientDataError", "NotReadyError", "RetrievalError",
-    "LinearModel", "PQCodebook", "build_score_lut", "pq_encode", "score_codes",
+    "LinearModel", "PQCodebook", "PQConfig", "build_score_lut", "learn_pq_codebook", "pq_encode", "score_codes",
     "RankedList", "RankerConfig", "Repository", "score_binary", "score_dense", "score_pq", "top_k",
     "FeatureStore", "OnlineTrainer", "TrainerConfig", "pegasos_step",
     "BatchTrainConfig", "train_batch", "hinge_objective",

@@ -86,6 +86,10 @@ SIGNATURES: dict[str, list] = {
     "otf_trainer_weights_ptr": [_vp, _P(_vp)],
     "otf_trainer_stream": [_vp, _P(_vp)],
     "otf_pq_encode": [_int, _vp, _i64, _i32, _vp, _i32, _i32, _i32, _vp, _int, _vp],
+    "otf_kmeans_create": [_int, _vp, _i64, _i32, _i32, _P(_vp)],
+    "otf_kmeans_load": [_vp, _vp],
+    "otf_kmeans_destroy": [_vp],
+    "otf_kmeans_step": [_vp, _vp, _vp, _vp, _P(_dbl)],
     "otf_group_unique_id": [_vp],
     "otf_group_create": [_int, _i32, _i32, _vp, _P(_vp)],
     "otf_group_destroy": [_vp],

@@ -1167,3 +1167,87 @@ int otf_group_rank(otf_group* g, otf_repo* r, const double* w, int32_t root, int
   if (out_rows) std::memcpy(out_rows, h + 3 * k_eff, (size_t)k_eff * 8);
   return OTF_OK;
 }
+
+// ---- k-means for PQ codebook learning (otf_kmeans.cu) ----------------------------------------
+struct otf_kmeans {
+  int device = 0;
+  int64_t n = 0;
+  int dim = 0, k = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf X, xx, C, cc, assign, best, counts, obj;
+  HostBuf h;  // staging for one step's outputs
+};
+
+int otf_kmeans_create(int device, const double* data, int64_t n, int32_t dim, int32_t k, otf_kmeans** out) {
+  if (!out) return fail(OTF_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (n <= 0 || dim <= 0 || k <= 0 || k > 256) return fail(OTF_ERR_CONFIG, "k-means needs n > 0, dim > 0, 1 <= k <= 256");
+  DeviceGuard g(device);
+  otf_kmeans* h = new otf_kmeans();
+  h->device = device; h->n = n; h->dim = dim; h->k = k;
+  int rc = OTF_OK;
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) rc = fail(OTF_ERR_CUDA, "cudaStreamCreate");
+  const size_t xb = (size_t)n * dim * 8;
+  if (!rc) rc = h->X.ensure(xb);
+  if (!rc) rc = h->xx.ensure((size_t)n * 8);
+  if (!rc) rc = h->C.ensure((size_t)k * dim * 8);
+  if (!rc) rc = h->cc.ensure((size_t)k * 8);
+  if (!rc) rc = h->assign.ensure((size_t)n * 4);
+  if (!rc) rc = h->best.ensure((size_t)n * 8);
+  if (!rc) rc = h->counts.ensure((size_t)k * 8);
+  if (!rc) rc = h->obj.ensure(8);
+  if (!rc) rc = h->h.ensure((size_t)n * 4 + (size_t)k * 8 + (size_t)k * dim * 8 + 8);
+  if (!rc && cudaMemcpyAsync(h->X.p, data, xb, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    rc = fail(OTF_ERR_CUDA, "k-means data upload");
+  if (!rc) rc = kmeans_row_norms(static_cast<const double*>(h->X.p), n, dim, static_cast<double*>(h->xx.p), h->stream);
+  if (!rc && cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(OTF_ERR_CUDA, "k-means setup");
+  if (rc) { otf_kmeans_destroy(h); return rc; }
+  *out = h;
+  return OTF_OK;
+}
+
+int otf_kmeans_load(otf_kmeans* h, const double* data) {
+  if (!h) return fail(OTF_ERR_CONFIG, "k-means handle is NULL");
+  DeviceGuard g(h->device);
+  OTF_CUDA(cudaMemcpyAsync(h->X.p, data, (size_t)h->n * h->dim * 8, cudaMemcpyHostToDevice, h->stream));
+  int rc = kmeans_row_norms(static_cast<const double*>(h->X.p), h->n, h->dim, static_cast<double*>(h->xx.p),
+                            h->stream);
+  if (rc) return rc;
+  OTF_CUDA(cudaStreamSynchronize(h->stream));
+  return OTF_OK;
+}
+
+int otf_kmeans_destroy(otf_kmeans* h) {
+  if (!h) return OTF_OK;
+  DeviceGuard g(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->X.release(); h->xx.release(); h->C.release(); h->cc.release(); h->assign.release(); h->best.release();
+  h->counts.release(); h->obj.release(); h->h.release();
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return OTF_OK;
+}
+
+int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* counts, double* objective) {
+  if (!h) return fail(OTF_ERR_CONFIG, "k-means handle is NULL");
+  DeviceGuard g(h->device);
+  const size_t cb = (size_t)h->k * h->dim * 8;
+  OTF_CUDA(cudaMemcpyAsync(h->C.p, centroids, cb, cudaMemcpyHostToDevice, h->stream));
+  int rc = kmeans_step(static_cast<const double*>(h->X.p), static_cast<const double*>(h->xx.p), h->n, h->dim, h->k,
+                       static_cast<double*>(h->C.p), static_cast<double*>(h->cc.p), static_cast<int32_t*>(h->assign.p),
+                       static_cast<double*>(h->best.p), static_cast<unsigned long long*>(h->counts.p),
+                       static_cast<double*>(h->obj.p), h->device, h->stream);
+  if (rc) return rc;
+  char* hs = static_cast<char*>(h->h.p);
+  const size_t ab = (size_t)h->n * 4, kb = (size_t)h->k * 8;
+  OTF_CUDA(cudaMemcpyAsync(hs, h->assign.p, ab, cudaMemcpyDeviceToHost, h->stream));
+  OTF_CUDA(cudaMemcpyAsync(hs + ab, h->counts.p, kb, cudaMemcpyDeviceToHost, h->stream));
+  OTF_CUDA(cudaMemcpyAsync(hs + ab + kb, h->C.p, cb, cudaMemcpyDeviceToHost, h->stream));
+  OTF_CUDA(cudaMemcpyAsync(hs + ab + kb + cb, h->obj.p, 8, cudaMemcpyDeviceToHost, h->stream));
+  OTF_CUDA(cudaStreamSynchronize(h->stream));
+  std::memcpy(assign, hs, ab);
+  std::memcpy(counts, hs + ab, kb);
+  std::memcpy(centroids, hs + ab + kb, cb);
+  std::memcpy(objective, hs + ab + kb + cb, 8);
+  return OTF_OK;
+}

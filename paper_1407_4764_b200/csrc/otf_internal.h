@@ -89,6 +89,11 @@ int launch_batch_train(const void* X, int dt, int64_t n_pos, int64_t n, int d, c
 int launch_hinge_objective(const void* X, int dt, int64_t n_pos, int64_t n, int d, const double* w,
                            double lam, double* out, cudaStream_t st);
 
+// k-means (otf_kmeans.cu)
+int kmeans_row_norms(const double* X, int64_t n, int Q, double* xx, cudaStream_t st);
+int kmeans_step(const double* X, const double* xx, int64_t n, int Q, int K, double* C, double* cc, int32_t* assign,
+                double* best, unsigned long long* counts, double* objective, int device, cudaStream_t st);
+
 // multi-GPU group (otf_group.cu)
 int group_unique_id(unsigned char* out128);
 int group_comm_create(int n_ranks, int rank, const unsigned char* id128, void** comm);

@@ -80,6 +80,28 @@ def main() -> None:
         g[f"pqenc_{name}_vecs"] = vecs
         g[f"pqenc_{name}_codes"] = rpq.pq_encode(book, vecs)
 
+    # ---- codebook learning (pq.py:116-203): learn_pq_codebook and _lloyd traces ----------------
+    for name, (n, d, q, k, iters, seed) in {"a": (3000, 16, 8, 64, 10, 3), "b": (1200, 12, 3, 16, 25, 4)}.items():
+        rng = np.random.default_rng(seed)
+        train = normalize_rows(rng.standard_normal((n, d))).astype(np.float32)
+        book = rpq.learn_pq_codebook(train, rpq.PQConfig(subdim=q, num_centroids=k, iterations=iters, seed=seed))
+        hist = book.objective_history
+        width = max(len(h) for h in hist)
+        g[f"km_{name}_train"] = train
+        g[f"km_{name}_cents"] = book.centroids
+        g[f"km_{name}_centering"] = book.centering
+        g[f"km_{name}_hist"] = np.array([h + [np.nan] * (width - len(h)) for h in hist])
+        g[f"km_{name}_hist_len"] = np.array([len(h) for h in hist])
+    hand_c, hand_h = rpq._lloyd(np.array([[0.0], [1.0], [2.0], [3.0]]), k=2, iterations=10,
+                                rng=np.random.default_rng(0), init=np.array([[0.0], [1000.0]]))
+    g["km_hand_cents"], g["km_hand_hist"] = hand_c, np.array(hand_h)
+    rng = np.random.default_rng(77)
+    data = rng.standard_normal((400, 3))
+    init = np.concatenate([data[:5], np.full((3, 3), 50.0)])  # three far centroids -> empty clusters
+    emp_c, emp_h = rpq._lloyd(data, k=8, iterations=15, rng=np.random.default_rng(1), init=init)
+    g["km_empty_data"], g["km_empty_init"] = data, init
+    g["km_empty_cents"], g["km_empty_hist"] = emp_c, np.array(emp_h)
+
     # ---- binary (ranker.py:78-94, binary.py:86-128) ----------------------------------------
     for name, (m, bits, n, seed) in {"b32": (8, 32, 200, 21), "b2048": (128, 2048, 300, 22),
                                      "b19": (8, 19, 150, 23), "b1024": (64, 1024, 300, 24)}.items():

@@ -453,3 +453,40 @@ def test_pq_encode_errors_and_empty(otf):
     with pytest.raises(otf.ConfigError):
         otf.pq_encode(book, np.zeros((5, 7), np.float32))
     assert otf.pq_encode(book, np.zeros((0, 6), np.float32)).shape == (0, 2)
+
+
+# ---- codebook learning (pq.py:116-203) -----------------------------------------------------------
+@pytest.mark.parametrize("name,q,k,iters,seed", [("a", 8, 64, 10, 3), ("b", 3, 16, 25, 4)])
+def test_learn_pq_codebook_matches_reference_golden(otf, golden, name, q, k, iters, seed):
+    """GPU Lloyd steps (assignment, objective, means) + host re-seeding reproduce the reference's
+    codebooks bit-for-bit and its objective histories to rounding (the BLAS dot order)."""
+    book = otf.learn_pq_codebook(golden[f"km_{name}_train"],
+                                 otf.PQConfig(subdim=q, num_centroids=k, iterations=iters, seed=seed))
+    np.testing.assert_array_equal(book.centroids, golden[f"km_{name}_cents"])
+    np.testing.assert_array_equal(book.centering, golden[f"km_{name}_centering"])
+    assert [len(h) for h in book.objective_history] == list(golden[f"km_{name}_hist_len"])
+    for m, h in enumerate(book.objective_history):
+        np.testing.assert_allclose(h, golden[f"km_{name}_hist"][m][:len(h)], rtol=1e-12)
+
+
+def test_lloyd_traces_match_reference(otf, golden):
+    from paper_1407_4764_b200.pq import _lloyd
+
+    c, h = _lloyd(np.array([[0.0], [1.0], [2.0], [3.0]]), 2, 10, np.random.default_rng(0),
+                  init=np.array([[0.0], [1000.0]]))  # forced empty cluster (tests/test_pq.py:47-56)
+    np.testing.assert_array_equal(c, golden["km_hand_cents"])
+    np.testing.assert_array_equal(h, golden["km_hand_hist"])
+    c, h = _lloyd(golden["km_empty_data"], 8, 15, np.random.default_rng(1), init=golden["km_empty_init"])
+    np.testing.assert_array_equal(c, golden["km_empty_cents"])
+    np.testing.assert_allclose(h, golden["km_empty_hist"], rtol=1e-12)
+    c, h = _lloyd(golden["km_empty_data"], 8, 0, np.random.default_rng(1), init=golden["km_empty_init"])
+    assert h == [] and np.array_equal(c, golden["km_empty_init"])
+
+
+def test_learn_pq_codebook_errors(otf):
+    with pytest.raises(otf.ConfigError):
+        otf.learn_pq_codebook(np.ones((10, 10), np.float32), otf.PQConfig(subdim=4, num_centroids=2))
+    with pytest.raises(otf.InsufficientDataError):
+        otf.learn_pq_codebook(np.ones((3, 4), np.float32), otf.PQConfig(subdim=2, num_centroids=8))
+    with pytest.raises(otf.InsufficientDataError):  # too few distinct sub-vectors
+        otf.learn_pq_codebook(np.ones((20, 4), np.float32), otf.PQConfig(subdim=2, num_centroids=4))

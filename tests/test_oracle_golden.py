@@ -147,3 +147,23 @@ def test_oracle_pq_encode_matches_reference(golden, name):
     codes, gap = O.pq_encode(golden[f"pqenc_{name}_cents"], golden[f"pqenc_{name}_vecs"])
     np.testing.assert_array_equal(codes, golden[f"pqenc_{name}_codes"])
     assert np.all(gap >= 0)
+
+
+@pytest.mark.parametrize("name,q,k,iters,seed", [("a", 8, 64, 10, 3), ("b", 3, 16, 25, 4)])
+def test_oracle_learn_pq_codebook_matches_reference(golden, name, q, k, iters, seed):
+    cents, hists, centering = O.learn_pq_codebook(golden[f"km_{name}_train"], q, k, iters, seed)
+    np.testing.assert_array_equal(cents, golden[f"km_{name}_cents"])
+    np.testing.assert_array_equal(centering, golden[f"km_{name}_centering"])
+    for m, h in enumerate(hists):
+        assert len(h) == golden[f"km_{name}_hist_len"][m]
+        np.testing.assert_allclose(h, golden[f"km_{name}_hist"][m][:len(h)], rtol=1e-12)
+
+
+def test_oracle_lloyd_traces(golden):
+    c, h = O.lloyd(np.array([[0.0], [1.0], [2.0], [3.0]]), 2, 10, np.random.default_rng(0),
+                   init=np.array([[0.0], [1000.0]]))
+    np.testing.assert_array_equal(c, golden["km_hand_cents"])
+    np.testing.assert_array_equal(h, golden["km_hand_hist"])
+    c, h = O.lloyd(golden["km_empty_data"], 8, 15, np.random.default_rng(1), init=golden["km_empty_init"])
+    np.testing.assert_array_equal(c, golden["km_empty_cents"])
+    np.testing.assert_allclose(h, golden["km_empty_hist"], rtol=1e-12)
