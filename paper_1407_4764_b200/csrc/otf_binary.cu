@@ -10,6 +10,12 @@
 // on its position. Parity with the reference's float32 sgemv is a tolerance.
 //
 // HBM roofline: n_bits/8 bytes per row (256 B for 2048-bit codes).
+#include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "otf_common.cuh"
 #include "otf_internal.h"
 
@@ -34,7 +40,7 @@ __global__ void __launch_bounds__(kBinThreads, 1)
 bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
                 const double* __restrict__ w, int n_bits, const double* __restrict__ partial_in,
                 double* __restrict__ partial_out, float* __restrict__ out,
-                uint32_t* __restrict__ ghist) {
+                uint32_t* __restrict__ ghist, const __grid_constant__ CUtensorMap map, int use_pf) {
   extern __shared__ __align__(16) unsigned char tabb[];  // 128 KB
   __shared__ uint32_t sh[kHistBins];
   for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
@@ -59,6 +65,15 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
   bool writer;
   const int slot = row_of_lane<R, 32>(lane, &writer);  // the row this lane finishes
   for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
+    // the warp's next R rows of THIS slice go to L2 now (one 2-D bulk prefetch: 128 B x R rows,
+    // row stride RB), so the next iteration's loads wait on L2 rather than HBM latency
+    if (use_pf && lane == 0) {
+      const int64_t nr = r0 + use_pf * nwarp * R;  // use_pf = prefetch distance in iterations
+      if (nr < n)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map), "r"(slice * 128),
+                     "r"((int)nr)
+                     : "memory");
+    }
     uint32_t wd[R];
     const uint8_t* rp = base + r0 * RB;
     if (r0 + R <= n) {
@@ -212,6 +227,29 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       cudaFuncSetAttribute((const void*)bin_score_bytes<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured[device & 63] = true;
     }
+    // tensor map over the codes (u8, RB x n) for the in-kernel L2 prefetch of the next tile
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    int use_pf = 0;
+    {
+      static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+      if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* fp = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+          enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
+      }
+      const cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)n};
+      const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+      const cuuint32_t box[2] = {128, 32};
+      const cuuint32_t estr[2] = {1, 1};
+      if (enc && !getenv("OTF_BIN_NO_PREFETCH") && n < (int64_t)0x7fffffff &&
+          enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        use_pf = 1;  // distance 1..3 iterations measured the same
+    }
     int64_t grid = sm_count(device);  // one 512-thread CTA per SM (128 KB table)
     const int64_t need = (n + (kBinThreads / 32) * 32 - 1) / ((kBinThreads / 32) * 32);
     if (need < grid) grid = need;
@@ -221,10 +259,10 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       double* pout = last ? nullptr : scratch;
       float* o = last ? out : nullptr;
       switch (row_bytes) {
-        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
-        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
-        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
-        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist); break;
+        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
+        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
+        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
+        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
       }
       OTF_LAUNCH_CHECK("bin_score_bytes");
     }
