@@ -366,11 +366,26 @@ def run_gpu(args, cfg):
 
     if multi:
         if world > 1:
-            raise SystemExit("c5b runs one replica per GPU; use --gpus 1")
+            # weak scaling: every rank scores its own rows under all classifiers; per classifier
+            # the k local candidates of every rank are all-gathered and merged exactly
+            g_sc = torch.empty((world, n_cls, k), dtype=torch.float64, device=dev)
+            g_ids = torch.empty((world, n_cls, k), dtype=torch.int64, device=dev)
+            f_ids = torch.empty((n_cls, k), dtype=torch.int64, device=dev)
+            f_sc = torch.empty((n_cls, k), dtype=torch.float64, device=dev)
+            f_got = C.c_int64()
 
         def step():
             _lib.check(lib.otf_repo_rank_many(repo.handle, _lib.tptr(W_dev), n_cls, k, _lib.tptr(m_ids),
                                               _lib.tptr(m_sc), C.byref(m_got), _lib.MEM_DEVICE, sp))
+            if world > 1:
+                dist.all_gather_into_tensor(g_sc, m_sc)
+                dist.all_gather_into_tensor(g_ids, m_ids)
+                c_sc = g_sc.transpose(0, 1).contiguous()    # (n_cls, world * k)
+                c_ids = g_ids.transpose(0, 1).contiguous()
+                for c in range(n_cls):
+                    _lib.check(lib.otf_top_k(local, _lib.tptr(c_sc[c]), _lib.F64, world * k, _lib.tptr(c_ids[c]), k,
+                                             _lib.tptr(f_ids[c]), _lib.tptr(f_sc[c]), None, C.byref(f_got),
+                                             _lib.MEM_DEVICE, sp))
     elif world > 1 and args.group == "native":
         # the library's own NCCL communicator (otf_group_*); the unique id travels over torch
         from paper_1407_4764_b200.distributed import NcclShardGroup
@@ -470,7 +485,14 @@ def run_gpu(args, cfg):
     # ---- end to end through the public API (host w in, host RankedList out) ---------------
     e2e_steps = max(3, min(args.steps, 200))
     model = otf.LinearModel(w, 1, 1)
-    if multi:
+    if multi and world > 1:
+        W_pin = torch.from_numpy(Wm).pin_memory()
+
+        def api():  # host W in (pinned H2D), exact global lists out (D2H) on every rank
+            W_dev.copy_(W_pin, non_blocking=True)
+            step()
+            return f_ids.cpu(), f_sc.cpu()
+    elif multi:
         models = [otf.LinearModel(wc, 1, 1) for wc in Wm]
         api = lambda: repo.rank_many(models, k)
     elif world > 1 and args.group == "native":
