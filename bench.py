@@ -580,6 +580,14 @@ def run_gpu(args, cfg):
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
+def profile_traffic(config):
+    prof = ROOT / "profiles" / f"ncu_{config}_summary.json"
+    try:
+        return json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def run_encode(args, cfg):
     """C3 ingest: pq_encode of the whole batch of device-resident vectors per step (one GPU per
     rank, each encodes its own rows). The kernel is FP32-FMA bound (K*Q fused multiply-adds per
@@ -676,7 +684,8 @@ def run_encode(args, cfg):
             "config": {"workload": cfg["workload"], "rows_per_gpu": n, "dim": dim, "blocks": M,
                        "centroids": K, "subdim": Q, "l2": "inputs (%.1f GB/GPU) larger than L2" % (n * dim * 4 / 1e9)},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                         "frac": achieved / FP32_PEAK_TFLOPS, "traffic": profile_traffic("c3e"),
+                         "traffic_unit": "DRAM bytes per launch (ncu)",
                          "kernel": "pq_encode_kernel<8>: 2*K*Q flop per vector and block (FFMA screening)",
                          "hbm_gbs": n * (dim * 4 + M) / (ms / 1e3) / 1e9,
                          "peak_source": "derived: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (no measured FP32 peak)"},

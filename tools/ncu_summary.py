@@ -58,10 +58,22 @@ def main(rep, out):
             rec["dram_bytes_total"] = rec["dram_bytes_read"] + rec.get("dram_bytes_write", 0.0)
         launches.append(rec)
     summary = {"source": rep, "launches": launches}
-    score = [l for l in launches if any(s in l["kernel"] for s in ("dense_score", "pq_scan", "bin_score", "multi_score"))]
+    names = ("dense_score", "pq_scan", "bin_score", "multi_score", "pq_encode_kernel")
+    score = [l for l in launches if any(s in l["kernel"] for s in names)]
     if score:
         summary["dram_bytes_per_launch"] = score[0].get("dram_bytes_total")
         summary["score_kernel"] = score[0]["kernel"]
+        # the binary scan is one launch per 128-byte slice: one scoring call = the consecutive
+        # slice launches (capture them together with -c <slices>)
+        if "bin_score_bytes" in score[0]["kernel"]:
+            i0 = launches.index(score[0])
+            run = [score[0]]
+            for l in launches[i0 + 1:]:
+                if "bin_score_bytes" not in l["kernel"]:
+                    break
+                run.append(l)
+            summary["dram_bytes_per_launch"] = sum(l.get("dram_bytes_total", 0.0) for l in run)
+            summary["score_launches_summed"] = len(run)
     with open(out, "w") as f:
         json.dump(summary, f, indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "launches"}))
