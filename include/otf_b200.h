@@ -214,6 +214,14 @@ int otf_trainer_set_weights(otf_trainer* tr, const double* w, int mem);
 int otf_trainer_weights_ptr(otf_trainer* tr, const double** out);
 /* The trainer's CUDA stream (high priority; runs concurrently with ranking). */
 int otf_trainer_stream(otf_trainer* tr, void** out);
+/* Snapshot publication without a host round trip (SURVEY.md §8b threading; the device side of
+ * trainer.py:161-173): copy the trainer's current w into the repository's snapshot buffer on the
+ * trainer stream (ordered after every step already enqueued) and make the repository's stream
+ * wait for it (CUDA event). The trainer keeps stepping on its own buffer meanwhile. */
+int otf_trainer_publish(otf_trainer* tr, otf_repo* repo);
+/* rank(k) under the last published snapshot (ranker.py:272-281), host outputs. */
+int otf_repo_rank_published(otf_repo* repo, int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+                            int64_t* out_n);
 
 /* ---- PQ codebook learning (learn_pq_codebook / _lloyd, pq.py:116-203) --------------------------
  * A handle keeps one block's float64 training sub-vectors (n, dim) on the device. Each step is

@@ -115,6 +115,7 @@ struct otf_repo {
   cudaStream_t stream = nullptr;
   std::mutex mu;                   // one call at a time per handle
   DevBuf w, w32, lut, scores, bins, outbuf, multi;  // multi: (<=64, n) float32 classifier scores
+  DevBuf wpub;  // the ranker's copy of the trainer's w (otf_trainer_publish)
   HostBuf h_w, h_out;
   TopkWs topk;
   TopkWs mtopk;  // segment workspace of rank_many (kept apart: graphs capture topk's pointers)
@@ -134,6 +135,7 @@ struct otf_trainer {
   int neg_dtype = OTF_F32;
   int64_t n_neg = 0;
   int64_t n_pos = 0, pos_cap = 0;
+  cudaEvent_t published = nullptr;  // recorded after each snapshot copy (otf_trainer_publish)
 };
 
 namespace {
@@ -204,7 +206,7 @@ void repo_free(otf_repo* r) {
   if (r->ids) cudaFree(r->ids);
   if (r->cents) cudaFree(r->cents);
   r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->bins.release(); r->outbuf.release();
-  r->multi.release();
+  r->multi.release(); r->wpub.release();
   r->h_w.release(); r->h_out.release();
   topk_ws_free(&r->topk);
   topk_ws_free(&r->mtopk);
@@ -945,6 +947,7 @@ int otf_trainer_destroy(otf_trainer* t) {
   if (t->stream) cudaStreamSynchronize(t->stream);
   t->w.release(); t->neg.release(); t->pos_pool.release(); t->pos_stage.release(); t->idx.release();
   t->h_stage.release(); t->h_idx.release();
+  if (t->published) cudaEventDestroy(t->published);
   if (t->stream) cudaStreamDestroy(t->stream);
   delete t;
   return OTF_OK;
@@ -1249,5 +1252,54 @@ int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* 
   std::memcpy(counts, hs + ab, kb);
   std::memcpy(centroids, hs + ab + kb, cb);
   std::memcpy(objective, hs + ab + kb + cb, 8);
+  return OTF_OK;
+}
+
+// ---- snapshot publication: trainer w -> ranker buffer on the device (SURVEY.md §8b threading) ----
+int otf_trainer_publish(otf_trainer* t, otf_repo* r) {
+  if (!t || !r) return fail(OTF_ERR_CONFIG, "trainer or repository is NULL");
+  if (t->device != r->device) return fail(OTF_ERR_CONFIG, "trainer and repository are on different devices");
+  if (t->dim != r->model_dim)
+    return fail(OTF_ERR_CONFIG, "store dim " + std::to_string(r->model_dim) + " does not match model dim " +
+                                    std::to_string(t->dim));
+  std::lock_guard<std::mutex> lt(t->mu);
+  std::lock_guard<std::mutex> lr(r->mu);
+  DeviceGuard g(t->device);
+  int rc = r->wpub.ensure((size_t)t->dim * 8);
+  if (rc) return rc;
+  if (!t->published) OTF_CUDA(cudaEventCreateWithFlags(&t->published, cudaEventDisableTiming));
+  // the copy is ordered after every step already enqueued on the trainer stream and before any
+  // later one; the ranker's stream waits for it (no host round trip, no host copy of w)
+  OTF_CUDA(cudaMemcpyAsync(r->wpub.p, t->w.p, (size_t)t->dim * 8, cudaMemcpyDeviceToDevice, t->stream));
+  OTF_CUDA(cudaEventRecord(t->published, t->stream));
+  OTF_CUDA(cudaStreamWaitEvent(r->stream, t->published, 0));
+  return OTF_OK;
+}
+
+int otf_repo_rank_published(otf_repo* r, int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
+                            int64_t* out_n) {
+  if (!r) return fail(OTF_ERR_CONFIG, "repository is NULL");
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  if (!r->wpub.p || r->wpub.bytes < (size_t)r->model_dim * 8)
+    return fail(OTF_ERR_NOT_READY, "no snapshot published yet");
+  int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  if (out_n) *out_n = k_eff;
+  if (k_eff == 0) return OTF_OK;
+  cudaStream_t st = r->stream;
+  const size_t bytes = (size_t)k_eff * 24;
+  int rc = r->outbuf.ensure(bytes);
+  if (!rc) rc = r->h_out.ensure(bytes);
+  if (rc) return rc;
+  int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
+  double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
+  if ((rc = rank_device(r, static_cast<const double*>(r->wpub.p), k_eff, d_ids, d_sc, d_rows, st))) return rc;
+  OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
+  OTF_CUDA(cudaStreamSynchronize(st));
+  const int64_t* h = static_cast<const int64_t*>(r->h_out.p);
+  std::memcpy(out_ids, h, (size_t)k_eff * 8);
+  std::memcpy(out_scores, h + k_eff, (size_t)k_eff * 8);
+  if (out_rows) std::memcpy(out_rows, h + 2 * k_eff, (size_t)k_eff * 8);
   return OTF_OK;
 }

@@ -340,6 +340,22 @@ class Repository:
             out.append(RankedList(ids[i].copy(), sc[i].copy(), model_version(m), produced_at, names))
         return out
 
+    def rank_published(self, k: int, produced_at: float = 0.0, model_version: int = 0) -> RankedList:
+        """rank(k) under the w an OnlineTrainer last published into this repository
+        (``OnlineTrainer.publish_to``): same list as ``rank(trainer.snapshot(), k)``."""
+        n = self.count
+        k_eff = max(0, min(int(k), n))
+        if k_eff == 0:
+            return _empty_list(model_version, produced_at, self.names)
+        out_ids = np.empty(k_eff, dtype=np.int64)
+        out_sc = np.empty(k_eff, dtype=np.float64)
+        out_rows = np.empty(k_eff, dtype=np.int64) if self.names is not None else None
+        got = C.c_int64(0)
+        _lib.check(_lib.load().otf_repo_rank_published(self._handle, k_eff, _lib.ptr(out_ids), _lib.ptr(out_sc),
+                                                       _lib.ptr(out_rows), C.byref(got)))
+        names = tuple(self.names[int(r)] for r in out_rows) if self.names is not None else None
+        return RankedList(out_ids, out_sc, model_version, produced_at, names)
+
     def rank(self, model, k: int, produced_at: float = 0.0) -> RankedList:
         w = self._weights(model)
         n = self.count

@@ -6,9 +6,11 @@ semantically, with the state where the GPU needs it:
     training step gathers its B/2 positives on the device instead of converting the whole pool to
     float64 on the host every step (trainer.py:100-102);
   * ``train_step`` runs one Pegasos kernel on the trainer's high-priority stream;
-  * ``rank_tick`` snapshots w (versioned exactly like trainer.py:161-173) and ranks the
-    GPU-resident repository; the publication carries the same CRC32 over the int64 ids /
-    float64 scores bytes as session.py:96-116.
+  * ``rank_tick`` publishes w from the trainer's buffer into the repository's ranking buffer on
+    the device (``OnlineTrainer.publish_to``: one device copy ordered on the trainer stream + a
+    CUDA event the ranker's stream waits on — no host round trip; versioned exactly like
+    trainer.py:161-173) and ranks the GPU-resident repository; the publication carries the same
+    CRC32 over the int64 ids / float64 scores bytes as session.py:96-116.
 ``run_simulated`` replays a session on a virtual clock with the reference's event order
 (feeds at (i+1)/rate, training every 1/steps_per_second from the first arrival, rank ticks
 every interval; feed < train < rank at equal times — session.py:237-290).
@@ -166,10 +168,12 @@ class QuerySession:
     def rank_tick(self, now: float) -> bool:
         """session.py:197-218: rank under the latest snapshot and publish the top k."""
         try:
-            model = self.trainer.snapshot()
+            # device-side snapshot: w goes from the trainer's buffer to the ranker's on the GPU
+            # (copy + event), versioned exactly like trainer.snapshot()
+            _, version = self.trainer.publish_to(self.repository)
         except NotReadyError:
             return False
-        ranked = self.repository.rank(model, self.cfg.ranker.k, produced_at=now)
+        ranked = self.repository.rank_published(self.cfg.ranker.k, produced_at=now, model_version=version)
         with self._lock:
             self._lists_published += 1
             pub = Publication.build(ranked, len(self.pool), self.trainer.iteration, self._lists_published)

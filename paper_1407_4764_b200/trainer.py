@@ -190,18 +190,35 @@ class OnlineTrainer:
         _lib.check(_lib.load().otf_trainer_weights_ptr(self._handle, C.byref(p)))
         return int(p.value or 0)
 
+    def _sync_version(self) -> None:
+        """(under _lock) version bumps only when the iterate moved (trainer.py:167-173)."""
+        if self._iteration != self._published_iteration:
+            self._version += 1
+            self._published_iteration = self._iteration
+            self._snap = None
+
     def snapshot(self) -> LinearModel:
         """trainer.py:161-173 — immutable copy; version bumps only when the iterate moved."""
         with self._lock:
             if self._iteration == 0:
                 raise NotReadyError("no training step has run yet")
-            if self._iteration != self._published_iteration or self._snap is None:
+            self._sync_version()
+            if self._snap is None:
                 w = np.empty(self._dim, dtype=np.float64)
                 _lib.check(_lib.load().otf_trainer_weights(self._handle, _lib.ptr(w), _lib.MEM_HOST))
-                self._version += 1
-                self._published_iteration = self._iteration
                 self._snap = LinearModel(w, self._iteration, self._version)
             return LinearModel(self._snap.weights.copy(), self._snap.iteration, self._snap.version)
+
+    def publish_to(self, repository) -> tuple[int, int]:
+        """The device-side snapshot: w goes straight into ``repository``'s ranking buffer (one
+        device copy + CUDA event, no host round trip); returns (iteration, version) with the
+        versioning of snapshot(). Rank it with ``repository.rank_published``."""
+        with self._lock:
+            if self._iteration == 0:
+                raise NotReadyError("no training step has run yet")
+            self._sync_version()
+            _lib.check(_lib.load().otf_trainer_publish(self._handle, repository.handle))
+            return self._iteration, self._version
 
 
 # -- fixed-set training (trainer.py:176-257) ------------------------------------------------------

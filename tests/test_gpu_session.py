@@ -39,3 +39,33 @@ def test_replay_is_bitwise_reproducible(otf, golden):
     _, a = run(otf, golden)
     _, b = run(otf, golden)
     assert [p.checksum for p in a] == [p.checksum for p in b]
+
+
+def test_device_snapshot_publication_equals_host_snapshot(otf, golden):
+    """OnlineTrainer.publish_to + Repository.rank_published (w copied trainer -> ranker on the
+    device, CUDA event, no host round trip) rank exactly like rank(trainer.snapshot()), with the
+    same version numbering; the trainer keeps its own buffer."""
+    import pytest as _pytest
+
+    repo = otf.Repository.dense(otf.FeatureStore(golden["sess_test_x"]))
+    tr = otf.OnlineTrainer(repo.model_dim, golden["sess_neg"], otf.TrainerConfig(lam=0.1, batch_size=16, seed=2))
+    with _pytest.raises(otf.NotReadyError):
+        tr.publish_to(repo)
+    tr.append_positives(golden["sess_feed"][:5])
+    for _ in range(7):
+        tr.step()
+    it, ver = tr.publish_to(repo)
+    a = repo.rank_published(25, produced_at=1.5, model_version=ver)
+    snap = tr.snapshot()
+    assert (snap.iteration, snap.version) == (it, ver)
+    b = repo.rank(snap, 25, produced_at=1.5)
+    assert list(a.ids) == list(b.ids) and np.array_equal(a.scores, b.scores)
+    assert a.model_version == b.model_version == ver
+    tr.step()  # a new iterate -> a new version; the published copy is unaffected until republished
+    c = repo.rank_published(25, model_version=ver)
+    assert list(c.ids) == list(a.ids)
+    it2, ver2 = tr.publish_to(repo)
+    assert (it2, ver2) == (it + 1, ver + 1)
+    small = otf.Repository.dense(otf.FeatureStore(np.ones((10, 16), np.float32)))
+    with _pytest.raises(otf.ConfigError):
+        tr.publish_to(small)
