@@ -49,6 +49,12 @@ constexpr int kMT = 128;          // rows per CTA tile
 constexpr int kKC = 32;           // K floats per chunk (128 bytes = one swizzle row)
 constexpr int kXStages = 8;       // X ring (freed by the split warps + the MMA commit)
 constexpr int kASlots = 8;        // TMEM ring of 32-column x_lo slots
+// The tensor core accumulates in float32 without round-to-nearest on every add: accumulated over
+// all of K (d = 4096) the error reached 0.9 of the reference tolerance. Restarting the
+// accumulation every 4 chunks (128 K values) and adding the group partials in float32 (RN) in the
+// epilogue brings it to numpy's own float32 sgemm level (0.055 vs 0.041 of the tolerance at
+// d = 4096; 0.155 vs 0.128 at d = 512) at ~1-3% of kernel time (tools/multi_err.py).
+constexpr int kGroupChunks = 4;
 constexpr int kTileX = kMT * kKC * 4;  // 16 KB
 constexpr int kMultiThreads = 512;
 constexpr int kTmemCols = 512;
@@ -149,6 +155,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // The tcgen05 / TMA / barrier instructions that differ between a single CTA and a pair.
 #define OTF_ELECT "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\t"
+
 template <int P>
 struct Ops;
 template <>
@@ -338,23 +345,28 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
     if (rank == 0) {
       const uint64_t wdesc0 = umma_desc_sw128(smem_u32(wring));
       const uint64_t xdesc0 = umma_desc_sw128(smem_u32(xring));
+      // accumulation restarts every kGroupChunks chunks in the other accumulator; the epilogue
+      // adds the group partials in float32 (round to nearest)
       uint32_t it = 0, j = 0;
-      for (int64_t t = unit; t < n_tiles; t += n_units, ++j) {
-        const int b = j & 1;
-        mbar_wait(&tmem_empty[b], ((j >> 1) & 1u) ^ 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem_base + b * 128;
-        for (int kc = 0; kc < kchunks; ++kc, ++it) {
-          const int s = it % C::kWStages, sx = it % kXStages, a = it % kASlots;
-          mbar_wait(&wfull[s], (it / C::kWStages) & 1u);  // W (both halves) landed
-          mbar_wait(&a_full[a], (it / kASlots) & 1u);     // X landed and x_lo in TMEM (both CTAs)
+      for (int64_t t = unit; t < n_tiles; t += n_units) {
+        for (int g0 = 0; g0 < kchunks; g0 += kGroupChunks, ++j) {
+          const int b = j & 1;
+          mbar_wait(&tmem_empty[b], ((j >> 1) & 1u) ^ 1u);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint64_t wd = wdesc0 + (uint64_t)((s * kTileW) >> 4);
-          O::mma_chunk(acc, xdesc0 + (uint64_t)((sx * kTileX) >> 4), tmem_base + kAccCols + a * 32, wd,
-                       wd + (uint64_t)((C::kW2Row * 128) >> 4), kc, smem_u32(&empty[sx]), smem_u32(&wempty[s]),
-                       smem_u32(&a_empty[a]));
+          const uint32_t acc = tmem_base + b * 128;
+          const int g1 = g0 + kGroupChunks < kchunks ? g0 + kGroupChunks : kchunks;
+          for (int kc = g0; kc < g1; ++kc, ++it) {
+            const int s = it % C::kWStages, sx = it % kXStages, a = it % kASlots;
+            mbar_wait(&wfull[s], (it / C::kWStages) & 1u);  // W (both halves) landed
+            mbar_wait(&a_full[a], (it / kASlots) & 1u);     // X landed and x_lo in TMEM (both CTAs)
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t wd = wdesc0 + (uint64_t)((s * kTileW) >> 4);
+            O::mma_chunk(acc, xdesc0 + (uint64_t)((sx * kTileX) >> 4), tmem_base + kAccCols + a * 32, wd,
+                         wd + (uint64_t)((C::kW2Row * 128) >> 4), kc - g0, smem_u32(&empty[sx]),
+                         smem_u32(&wempty[s]), smem_u32(&a_empty[a]));
+          }
+          O::commit(&tmem_full[b]);
         }
-        O::commit(&tmem_full[b]);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -362,29 +374,35 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
     const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
     const uint32_t te = O::leader_bar(&tmem_empty[0]);
     uint32_t j = 0;
-    for (int64_t t = unit; t < n_tiles; t += n_units, ++j) {
-      const int b = j & 1;
-      mbar_wait(&tmem_full[b], (j >> 1) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int64_t t = unit; t < n_tiles; t += n_units) {
       const int64_t row = t * P * kMT + rank * kMT + 32 * q + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + b * 128;
+      float sum[64];
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t h[16], l[16];
-        tmem_ld16(taddr + c0, h);
-        tmem_ld16(taddr + 64 + c0, l);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < n) {
+      for (int c = 0; c < 64; ++c) sum[c] = 0.f;
+      for (int g0 = 0; g0 < kchunks; g0 += kGroupChunks, ++j) {
+        const int b = j & 1;
+        mbar_wait(&tmem_full[b], (j >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + b * 128;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int c = c0 + u;
-            if (c < n_cls) out[(int64_t)c * n + row] = __fadd_rn(__uint_as_float(h[u]), __uint_as_float(l[u]));
-          }
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t h[16], l[16];
+          tmem_ld16(taddr + c0, h);
+          tmem_ld16(taddr + 64 + c0, l);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            sum[c0 + u] = __fadd_rn(sum[c0 + u], __fadd_rn(__uint_as_float(h[u]), __uint_as_float(l[u])));
         }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) O::arrive_leader(te + b * 8);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) O::arrive_leader(te + b * 8);
+      if (row < n) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c < n_cls) out[(int64_t)c * n + row] = sum[c];
+      }
     }
   } else if (warp >= 8) {
     // ---------------- split: x_lo of row r into this CTA's TMEM slot ----------------
@@ -407,8 +425,9 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
           const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 4; ++u) {
             lo[4 * c + u] = __float_as_uint(__fsub_rn(e[u], __uint_as_float(__float_as_uint(e[u]) & 0xFFFFE000u)));
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // read; the MMA commit frees the tile (x_hi)

@@ -29,9 +29,10 @@ def test_score_many_matches_dense(otf, n, d, c):
     assert S.shape == (c, n) and S.dtype == np.float32
     ex = exact(x, W).T
     mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
-    # TF32 x3: dropped lo*lo and TF32 rounding of the lo parts (~2^-20 relative per product)
-    # plus float32 accumulation in the tensor core
-    assert np.all(np.abs(S - ex) <= 2.0 ** -18 * mag + np.spacing(np.abs(S)) + 1e-30)
+    # TF32 x3: dropped lo*lo and TF32 truncation of the lo parts (<= 2^-21 relative per product),
+    # float32 accumulation restarted every 128 K values (measured max 2^-22 of mag, numpy's own
+    # float32 sgemm: 2^-22.3) -> a 4x margin
+    assert np.all(np.abs(S - ex) <= 2.0 ** -20 * mag + np.spacing(np.abs(S)) + 1e-30)
     for i in range(min(c, 5)):
         ref = O.score_dense(W[i], x)
         assert np.max(np.abs(S[i].astype(np.float64) - ref)) <= 1e-6 * np.linalg.norm(W[i]) * 1.0001
@@ -88,8 +89,8 @@ def test_single_cta_path_matches_pair_path(otf, monkeypatch, n, d, c):
     ex = exact(x, W).T
     mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
     for S in (S_pair, S_single):
-        assert np.all(np.abs(S - ex) <= 2.0 ** -18 * mag + np.spacing(np.abs(S)) + 1e-30)
-    assert np.all(np.abs(S_pair - S_single) <= 2.0 ** -17 * mag + 2 * np.spacing(np.abs(S_pair)) + 1e-30)
+        assert np.all(np.abs(S - ex) <= 2.0 ** -20 * mag + np.spacing(np.abs(S)) + 1e-30)
+    assert np.all(np.abs(S_pair - S_single) <= 2.0 ** -19 * mag + 2 * np.spacing(np.abs(S_pair)) + 1e-30)
 
 
 @pytest.mark.parametrize("n,d,c,k", [(50_000, 64, 64, 1000), (3000, 32, 40, 3000), (9000, 96, 5, 8500),
