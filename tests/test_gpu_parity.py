@@ -490,3 +490,32 @@ def test_learn_pq_codebook_errors(otf):
         otf.learn_pq_codebook(np.ones((3, 4), np.float32), otf.PQConfig(subdim=2, num_centroids=8))
     with pytest.raises(otf.InsufficientDataError):  # too few distinct sub-vectors
         otf.learn_pq_codebook(np.ones((20, 4), np.float32), otf.PQConfig(subdim=2, num_centroids=4))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_top_k_randomised_against_oracle(otf, seed):
+    """Randomised top_k cases (sizes, k around the candidate cap, dtypes, tie densities, signed
+    zeros, shuffled / huge ids): ids and float64 scores must equal the oracle's."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([1, 7, 1000, 8191, 8193, 50_000, 300_000]))
+    k = int(rng.choice([0, 1, 17, 1000, 8192, 8193, n, n + 5]))
+    dtype = np.float32 if rng.random() < 0.6 else np.float64
+    kind = rng.choice(["normal", "few", "ties", "zeros", "const"])
+    if kind == "normal":
+        s = rng.standard_normal(n)
+    elif kind == "few":
+        s = rng.integers(-3, 4, n) / 7.0
+    elif kind == "ties":
+        s = np.round(rng.standard_normal(n) * 20) / 20
+    elif kind == "zeros":
+        s = np.where(rng.random(n) < 0.5, 0.0, -0.0) * (rng.random(n) < 0.9) + (rng.random(n) < 0.1) * rng.standard_normal(n)
+    else:
+        s = np.full(n, 1.25)
+    s = s.astype(dtype)
+    ids = None
+    if rng.random() < 0.5:
+        ids = rng.permutation(n).astype(np.int64) * int(rng.choice([1, 3, 1 << 40])) + int(rng.integers(0, 1000))
+    r = otf.top_k(s, k, ids=ids)
+    o_ids, o_sc, _ = O.top_k(s, k, ids)
+    np.testing.assert_array_equal(r.ids, o_ids)
+    np.testing.assert_array_equal(r.scores, o_sc)
