@@ -584,14 +584,12 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   return rc;
 }
 
-int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* ids_dev,
-                        double* scores_dev, int64_t* rows_dev, void* stream) {
-  std::lock_guard<std::mutex> lk(r->mu);
-  DeviceGuard g(r->device);
-  int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
-  if (k_eff == 0) return OTF_OK;
-  cudaStream_t st = pick_stream(r->stream, stream);
-  const void* key[6] = {w_dev, ids_dev, scores_dev, rows_dev, stream, nullptr};
+namespace {
+// rank(k) for a device w through the repository's cached CUDA graph (captured on the first call
+// for a given (w, outputs, stream, k), replayed afterwards). Caller holds r->mu.
+int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* ids_dev, double* scores_dev,
+                      int64_t* rows_dev, cudaStream_t st) {
+  const void* key[6] = {w_dev, ids_dev, scores_dev, rows_dev, st, nullptr};
   bool hit = r->gexec && r->g_k == k_eff;
   for (int i = 0; i < 5 && hit; ++i) hit = key[i] == r->g_key[i];
   if (!hit) {
@@ -604,6 +602,7 @@ int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* id
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
     if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
     if (rc) return rc;
+    OTF_CUDA(cudaStreamSynchronize(st));  // allocations above must not race the capture
     cudaStream_t cap;
     OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     OTF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
@@ -622,6 +621,16 @@ int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* id
   OTF_CUDA(cudaGraphLaunch(r->gexec, st));
   count_launch(3);
   return OTF_OK;
+}
+}  // namespace
+
+int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* ids_dev,
+                        double* scores_dev, int64_t* rows_dev, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  if (k_eff == 0) return OTF_OK;
+  return rank_graph_locked(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, pick_stream(r->stream, stream));
 }
 
 // ---- stateless primitives ----------------------------------------------------------------------
@@ -1294,7 +1303,8 @@ int otf_repo_rank_published(otf_repo* r, int64_t k, int64_t* out_ids, double* ou
   int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
   double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
-  if ((rc = rank_device(r, static_cast<const double*>(r->wpub.p), k_eff, d_ids, d_sc, d_rows, st))) return rc;
+  // the live ranker re-ranks every tau with a new w in the same buffer: one graph replay per tick
+  if ((rc = rank_graph_locked(r, static_cast<const double*>(r->wpub.p), k_eff, d_ids, d_sc, d_rows, st))) return rc;
   OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
   OTF_CUDA(cudaStreamSynchronize(st));
   const int64_t* h = static_cast<const int64_t*>(r->h_out.p);
