@@ -294,7 +294,7 @@ int64_t otf_launch_count(void) { return g_launches.load(); }
 
 const char* otf_kernel_names(void) {
   return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;pq_scan16_xor;"
-         "pq_scan_generic;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
+         "pq_scan_generic;pq_scan16_f32bins;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
          "bin_hamming;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
          "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local";
 }

@@ -17,6 +17,7 @@
 // HBM roofline: M bytes per row (16 B for C3). The LUT (M*256*8 B) lives in shared memory;
 // the scan is shared-memory-lookup bound for M=16.
 #include <algorithm>
+#include <cstdlib>
 
 #include "otf_common.cuh"
 #include "otf_internal.h"
@@ -296,13 +297,21 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
   const char* lutb = reinterpret_cast<const char*>(lut);
   const uint4* C4 = reinterpret_cast<const uint4*>(codes);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
-  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * ROWS; base < n;
-       base += stride) {
+  // software pipeline: the next batch of ROWS code rows is in flight while this one is scored
+  uint4 nu[ROWS];
+  int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * ROWS;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int64_t row = base + 32 * i + lane;
+    nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+  }
+  for (; base < n; base += stride) {
     uint4 u[ROWS];
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
-      const int64_t row = base + 32 * i + lane;
-      u[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+      u[i] = nu[i];
+      const int64_t row = base + stride + 32 * i + lane;
+      nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
@@ -361,6 +370,144 @@ static int launch_scan16(const uint8_t* codes, int64_t n, const float* cents, co
   return OTF_OK;
 }
 
+// ---- M == 16 rank path: float32 screening, exact bins -----------------------------------------
+// The rank path needs only each row's 16-bit score bin (the top-k recomputes the candidates'
+// exact float64 scores, otf_topk.cu PqBinSrc), and a bin is a monotone function of the score.
+// So each row is first summed from a float32 copy of the LUT: |s32 - s64| <= eps with
+// eps = 2^-20 * sum_m max_j |LUT[m][j]| (entries rounded to float32: 2^-24 each, a depth-4
+// float32 tree: 4 * 2^-24 of the sum, numpy's float64 tree: negligible — a >3x margin). If
+// [s32 - eps, s32 + eps] (outward-rounded) lies inside one bin, that IS the bin of the exact
+// score; otherwise (near a bin edge, or non-finite LUT) the row's exact float64 score is
+// computed with numpy's pairwise order from the float64 LUT, as in pq_scan16_xor.
+// Shared-memory line j (256 B) holds the float64 entries (m, j) at bytes m*8 and two float32
+// copies at 128 + 64*c + 4*m. Lane l reads sub-code t ^ (l & 15) at step t from copy
+// (l >> 4): 32 lanes hit 32 different banks (one wavefront per LDS.32), and the whole
+// address is ONE byte_perm (code byte -> bits 8..15, a per-lane constant in bits 0..7).
+constexpr int kScanF32Threads = 512;
+constexpr size_t kScanF32Smem = 256 * 256 + kHistBins * sizeof(uint32_t) + 32 * sizeof(uint32_t);
+
+template <int ROWS>
+__global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const uint8_t* __restrict__ codes, int64_t n,
+                                                                     const double* __restrict__ lut_g, int K,
+                                                                     uint16_t* __restrict__ bins_out,
+                                                                     uint32_t* __restrict__ ghist) {
+  extern __shared__ __align__(256) unsigned char sm[];  // [256 lines x 256 B][hist][m maxima]
+  uint32_t* sh = reinterpret_cast<uint32_t*>(sm + 65536);
+  uint32_t* smax = sh + kHistBins;
+  if (threadIdx.x < 16) smax[threadIdx.x] = 0u;
+  hist_zero(sh);
+  __syncthreads();
+  {
+    // thread t always handles sub-quantizer m = t & 15 (blockDim = 512): 16 lanes fill one
+    // 128-byte run of a line, and the per-m maxima need one atomic per thread
+    const int m = threadIdx.x & 15;
+    uint32_t mx = 0u;
+    constexpr int kPer = 16 * 256 / kScanF32Threads;
+    double vs[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {  // all loads in flight before the first store
+      const int j = (threadIdx.x + i * kScanF32Threads) >> 4;
+      vs[i] = j < K ? lut_g[m * K + j] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int j = (threadIdx.x + i * kScanF32Threads) >> 4;
+      const double v = vs[i];
+      unsigned char* line = sm + (j << 8);
+      *reinterpret_cast<double*>(line + 8 * m) = v;
+      const float f = __double2float_rn(v);
+      *reinterpret_cast<float*>(line + 128 + 4 * m) = f;
+      *reinterpret_cast<float*>(line + 192 + 4 * m) = f;
+      // |v| as float rounded up: non-negative floats (and NaN above inf) order like their bits
+      mx = max(mx, __float_as_uint(fabsf(__double2float_ru(fabs(v)))));
+    }
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    if ((threadIdx.x & 31) < 16) atomicMax(&smax[m], mx);
+  }
+  __syncthreads();
+  float eps;
+  {
+    double e = 0.0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) e += (double)__uint_as_float(smax[m]);
+    eps = __double2float_ru(e * 0x1p-20);  // NaN/inf when the LUT is not finite
+    eps = fmaxf(eps, 0x1p-140f);  // absolute floor: float32 underflow of tiny entries
+  }
+  const bool screen = eps <= 3.0e38f;  // false: every row takes the exact path
+  const int lane = threadIdx.x & 31;
+  const uint32_t s = lane & 15;
+  // per step pair u: K word [offset of table 2u^s, offset of table (2u+1)^s, 0, 0] (copy lane>>4)
+  // and per t&3 the selector [K byte t&1, byte (t^s)&3 of the permuted word -> bits 8..15, 0, 0]
+  uint32_t kw[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t c = 128u | ((uint32_t)(lane >> 4) << 6);
+    kw[u] = (c | (((uint32_t)(2 * u) ^ s) << 2)) | ((c | (((uint32_t)(2 * u + 1) ^ s) << 2)) << 8);
+  }
+  uint32_t sel[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sel[q] = 0x7604u | (uint32_t)(q & 1) | ((((uint32_t)q ^ s) & 3u) << 4);
+  const uint4* C4 = reinterpret_cast<const uint4*>(codes);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
+  // software pipeline: the next batch of ROWS code rows is in flight while this one is scored
+  uint4 nu[ROWS];
+  int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * ROWS;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int64_t row = base + 32 * i + lane;
+    nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+  }
+  for (; base < n; base += stride) {
+    uint4 u[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      u[i] = nu[i];
+      const int64_t row = base + stride + 32 * i + lane;
+      nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const int64_t row = base + 32 * i + lane;
+      const bool active = row < n;
+      // word t>>2 of the permuted row = word (t>>2) ^ (s>>2) of the code row
+      const uint32_t x0 = u[i].x, x1 = u[i].y, x2 = u[i].z, x3 = u[i].w;
+      const uint32_t t0 = sel_u32(s & 8, x2, x0), t1 = sel_u32(s & 8, x3, x1);
+      const uint32_t t2 = sel_u32(s & 8, x0, x2), t3 = sel_u32(s & 8, x1, x3);
+      const uint32_t wd[4] = {sel_u32(s & 4, t1, t0), sel_u32(s & 4, t0, t1), sel_u32(s & 4, t3, t2),
+                              sel_u32(s & 4, t2, t3)};
+      float b[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        b[t] = *reinterpret_cast<const float*>(sm + __byte_perm(wd[t >> 2], kw[t >> 1], sel[t & 3]));
+      float r[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) r[t] = __fadd_rn(b[t], b[t + 8]);
+      const float s32 = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                                  __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+      uint32_t bin = hist_bin(__fsub_rd(s32, eps));
+      const bool exact = !screen || bin != hist_bin(__fadd_ru(s32, eps));
+      if (exact) {  // rare: the exact float64 score decides the bin (numpy's pairwise order)
+        const uint32_t xw[4] = {x0, x1, x2, x3};
+        double a[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m)
+          a[m] = *reinterpret_cast<const double*>(sm + (((xw[m >> 2] >> (8 * (m & 3))) & 0xffu) << 8) + 8 * m);
+        double rr[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
+        bin = hist_bin(__dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                                 __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7]))));
+      }
+      if (active) bins_out[row] = (uint16_t)bin;
+      if (ghist) hist_add(sh, active, bin);
+    }
+  }
+  if (ghist) {
+    __syncthreads();
+    hist_flush(sh, ghist);
+  }
+}
+
 bool pq_fast_path(int M, const uint8_t* codes) {
   return (((uintptr_t)codes) & 15) == 0 && (M == 4 || M == 8 || M == 16 || M == 32);
 }
@@ -370,7 +517,23 @@ bool pq_bins_path(int M, const uint8_t* codes) { return M == 16 && pq_fast_path(
 int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
                         uint32_t* hist, int device, cudaStream_t st) {
   if (n <= 0) return OTF_OK;
-  return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
+  static const bool f64_bins = getenv("OTF_PQ_F64_BINS") != nullptr;  // A/B switch (tools/)
+  if (f64_bins) return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
+  constexpr int ROWS = 4;  // 8 measured slower (128 registers, same occupancy)
+  auto fn = pq_scan16_f32bins<ROWS>;
+  static int per_sm[64] = {0};
+  if (!per_sm[device & 63]) {
+    OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanF32Smem));
+    int b = 0;
+    OTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kScanF32Threads, kScanF32Smem));
+    per_sm[device & 63] = b > 0 ? b : 1;
+  }
+  int64_t grid = (int64_t)per_sm[device & 63] * sm_count(device);
+  const int64_t need = (n + kScanF32Threads * ROWS - 1) / (kScanF32Threads * ROWS);
+  if (need < grid) grid = need;
+  fn<<<(int)grid, kScanF32Threads, kScanF32Smem, st>>>(codes, n, lut, K, bins, hist);
+  OTF_LAUNCH_CHECK("pq_scan16_f32bins");
+  return OTF_OK;
 }
 
 // Scores n code rows. Fast path: the LUT is built in-kernel from (cents, w) when cents is
