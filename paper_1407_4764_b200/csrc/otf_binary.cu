@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(kBinThreads, 1)
 bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
                 const double* __restrict__ w, int n_bits, const double* __restrict__ partial_in,
                 double* __restrict__ partial_out, float* __restrict__ out,
-                uint32_t* __restrict__ ghist, const __grid_constant__ CUtensorMap map, int use_pf) {
+                uint32_t* __restrict__ ghist, const __grid_constant__ CUtensorMap map, int use_pf,
+                uint16_t* __restrict__ cmax) {
   extern __shared__ __align__(16) unsigned char tabb[];  // 128 KB
   __shared__ uint32_t sh[kHistBins];
   for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
@@ -105,6 +106,10 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
       const float sc = __double2float_rn(total);
       if (active) out[row] = sc;
       if (ghist) hist_add(sh, active, hist_bin(sc));
+      if (cmax) {  // the warp's R consecutive rows are one top-k chunk
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, active ? hist_bin(sc) : 0u);
+        if (lane == 0) cmax[r0 / R] = (uint16_t)wm;
+      }
     } else if (active) {
       partial_out[row] = total;
     }
@@ -213,7 +218,8 @@ bool bin_bytes_path(int n_bits, const uint8_t* codes) {
 
 // w: float64 model (device); cast to float32 in-kernel (ranker.py:89). hist: see dense.
 int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
-                     uint32_t* hist, double* scratch, int device, cudaStream_t st) {
+                     uint32_t* hist, double* scratch, int device, cudaStream_t st, uint16_t* cmax,
+                     int* clog) {
   if (n <= 0) return OTF_OK;
   const int row_bytes = (n_bits + 7) / 8;
   if (bin_bytes_path(n_bits, codes) && (row_bytes == 128 || scratch != nullptr)) {
@@ -259,13 +265,14 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       double* pout = last ? nullptr : scratch;
       float* o = last ? out : nullptr;
       switch (row_bytes) {
-        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
-        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
-        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
-        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf); break;
+        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
+        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
+        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
+        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
       }
       OTF_LAUNCH_CHECK("bin_score_bytes");
     }
+    if (cmax && clog) *clog = 5;  // 32 rows per chunk
     return OTF_OK;
   }
   int64_t grid = (n + 7) / 8;

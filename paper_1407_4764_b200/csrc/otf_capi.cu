@@ -232,11 +232,12 @@ int stage_w(otf_repo* r, const double* w, int mem, cudaStream_t st, const double
 }
 
 // Scores every row of r into `out` (device). hist (nullable) receives the coarse histogram.
-int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStream_t st) {
+int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStream_t st,
+               uint16_t* cmax = nullptr, int* clog = nullptr) {
   int rc = OTF_OK;
   if (r->kind == OTF_KIND_DENSE)
     return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dw,
-                              static_cast<float*>(out), hist, r->device, st);
+                              static_cast<float*>(out), hist, r->device, st, cmax, clog);
   if (r->kind == OTF_KIND_PQ) {
     // the (M, K) float64 LUT is built once per query (one thread per entry), then every scan
     // CTA copies it into shared memory instead of re-deriving it
@@ -251,7 +252,7 @@ int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStr
   if ((rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(double)))) return rc;
   return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, dw,
                           static_cast<float*>(out), hist, static_cast<double*>(r->bins.p), r->device,
-                          st);
+                          st, cmax, clog);
 }
 
 int score_dtype(const otf_repo* r) { return r->kind == OTF_KIND_PQ ? OTF_F64 : OTF_F32; }
@@ -270,18 +271,31 @@ int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, doub
     if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double)))) return rc;
     if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st)))
       return rc;
+    if ((rc = topk_cmax_ensure(&r->topk, r->n))) return rc;
+    int clog = -1;
     if ((rc = launch_pq_scan_bins(codes, r->n, static_cast<const double*>(r->lut.p), r->K,
-                                  static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st)))
+                                  static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st,
+                                  r->topk.cmax, &clog)))
       return rc;
-    return launch_topk_pq_bins(static_cast<const uint16_t*>(r->bins.p), codes, r->M,
-                               static_cast<const double*>(r->lut.p), r->K, r->n, r->ids, r->id_base,
-                               k_eff, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows,
-                               r->device, st);
+    r->topk.clog = clog;
+    rc = launch_topk_pq_bins(static_cast<const uint16_t*>(r->bins.p), codes, r->M,
+                             static_cast<const double*>(r->lut.p), r->K, r->n, r->ids, r->id_base,
+                             k_eff, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows,
+                             r->device, st);
+    r->topk.clog = -1;
+    return rc;
   }
   const bool fuse = k_eff < r->n;
-  if ((rc = score_into(r, dw, r->scores.p, fuse ? r->topk.hist : nullptr, st))) return rc;
-  return launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, fuse,
-                     ids, scores, rows, r->device, st);
+  int clog = -1;
+  if (fuse && (rc = topk_cmax_ensure(&r->topk, r->n))) return rc;
+  if ((rc = score_into(r, dw, r->scores.p, fuse ? r->topk.hist : nullptr, st, fuse ? r->topk.cmax : nullptr,
+                       &clog)))
+    return rc;
+  r->topk.clog = clog;
+  rc = launch_topk(r->scores.p, score_dtype(r), r->n, r->ids, r->id_base, k_eff, &r->topk, fuse, ids, scores,
+                   rows, r->device, st);
+  r->topk.clog = -1;
+  return rc;
 }
 
 }  // namespace
@@ -601,6 +615,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
     if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
     if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
+    if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
     if (rc) return rc;
     OTF_CUDA(cudaStreamSynchronize(st));  // allocations above must not race the capture
     cudaStream_t cap;

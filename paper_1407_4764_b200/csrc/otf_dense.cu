@@ -40,7 +40,8 @@ template <int CPL, int R>
 __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restrict__ X, int64_t n,
                                                            const double* __restrict__ w,
                                                            float* __restrict__ out,
-                                                           uint32_t* __restrict__ ghist) {
+                                                           uint32_t* __restrict__ ghist,
+                                                           uint16_t* __restrict__ cmax) {
   const int lane = threadIdx.x & 31;
   __shared__ float4 wr[32 * CPL];
   __shared__ uint32_t sh[kHistBins];
@@ -88,6 +89,10 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
     const float s = __double2float_rn(p[0]);
     if (active) out[row] = s;
     if (ghist) hist_add(sh, active, hist_bin(s));
+    if (R > 1 && cmax) {  // the warp's R consecutive rows are one top-k chunk
+      const uint32_t wm = __reduce_max_sync(0xffffffffu, active ? hist_bin(s) : 0u);
+      if (lane == 0) cmax[r0 / R] = (uint16_t)wm;
+    }
   }
   if (ghist) {
     __syncthreads();
@@ -136,13 +141,15 @@ static int grid_for(const void* fn, int threads, int device) {
 
 template <int CPL, int R>
 static int launch_fast(const float* X, int64_t n, const double* w, float* out, uint32_t* hist,
-                       int device, cudaStream_t st) {
+                       int device, cudaStream_t st, uint16_t* cmax, int* clog) {
   auto fn = dense_score_fast<CPL, R>;
   int grid = grid_for((const void*)fn, 256, device);
   const int64_t need = (n + (8 * R) - 1) / (8 * R);  // 8 warps per block
   if (need < grid) grid = (int)(need > 0 ? need : 1);
-  fn<<<grid, 256, 0, st>>>(X, n, w, out, hist);
+  if (R < 8) cmax = nullptr;  // chunks of >= 8 rows only (topk_cmax_ensure)
+  fn<<<grid, 256, 0, st>>>(X, n, w, out, hist, cmax);
   OTF_LAUNCH_CHECK("dense_score_fast");
+  if (cmax && clog) *clog = 3;  // R == 8
   return OTF_OK;
 }
 
@@ -150,17 +157,17 @@ static int launch_fast(const float* X, int64_t n, const double* w, float* out, u
 // 16-byte aligned for the fast path (all device buffers this library allocates are).
 // hist (nullable): kHistBins counters (zero on entry) receiving the coarse score histogram.
 int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
-                       uint32_t* hist, int device, cudaStream_t st) {
+                       uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax, int* clog) {
   if (n <= 0) return OTF_OK;
   const bool aligned = (((uintptr_t)X) & 15) == 0;
   if (aligned && d % 128 == 0) {
     switch (d / 128) {
-      case 1: return launch_fast<1, 8>(X, n, w, out, hist, device, st);
-      case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st);
-      case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st);
-      case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st);
-      case 16: return launch_fast<16, 1>(X, n, w, out, hist, device, st);
-      case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st);
+      case 1: return launch_fast<1, 8>(X, n, w, out, hist, device, st, cmax, clog);
+      case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st, cmax, clog);
+      case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st, cmax, clog);
+      case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st, cmax, clog);
+      case 16: return launch_fast<16, 1>(X, n, w, out, hist, device, st, cmax, clog);
+      case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st, cmax, clog);
       default: break;
     }
   }

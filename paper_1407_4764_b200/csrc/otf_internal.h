@@ -9,8 +9,11 @@ namespace otf {
 // histogram (zero on entry) that receives the coarse score histogram for launch_topk.
 
 // dense (otf_dense.cu)
+// cmax (nullable): per-chunk maximum score bins for the top-k gather; *clog is set to log2 of
+// the chunk size when the kernel wrote them, else left at -1.
 int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
-                       uint32_t* hist, int device, cudaStream_t st);
+                       uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax = nullptr,
+                       int* clog = nullptr);
 
 // pq (otf_pq.cu)
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
@@ -25,7 +28,8 @@ bool pq_fast_path(int M, const uint8_t* codes);
 // M == 16 fast path can emit 16-bit score bins instead of float64 scores (rank path).
 bool pq_bins_path(int M, const uint8_t* codes);
 int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
-                        uint32_t* hist, int device, cudaStream_t st);
+                        uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax = nullptr,
+                        int* clog = nullptr);
 // fast path builds the LUT in-kernel from (cents, w); the generic path reads `lut`.
 int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, const double* w,
                    const double* lut, int K, int Q, double* out, uint32_t* hist, int device,
@@ -36,7 +40,8 @@ int launch_pq_scan(const uint8_t* codes, int64_t n, int M, const float* cents, c
 // row has more than one slice (> 1024 bits); otherwise the generic kernel runs.
 bool bin_bytes_path(int n_bits, const uint8_t* codes);
 int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* w, float* out,
-                     uint32_t* hist, double* scratch, int device, cudaStream_t st);
+                     uint32_t* hist, double* scratch, int device, cudaStream_t st,
+                     uint16_t* cmax = nullptr, int* clog = nullptr);
 int launch_bin_unpack(const uint8_t* codes, int64_t n, int n_bits, float* out, int device,
                       cudaStream_t st);
 int launch_binarize(const double* U, const float* mu, int m, int n_bits, const double* X,
@@ -56,7 +61,14 @@ struct TopkWs {
   int64_t cap = 0;                // power of two >= max(k_eff, kCandCap), per segment
   int n_seg = 0;                  // segments the counters are laid out for
   size_t slots = 0;               // allocated candidate slots (n_seg * cap)
+  // chunk maxima (optional, single segment): cmax[c] = max bin of rows [c << clog, (c+1) << clog),
+  // written by the scoring kernel of the same query; clog < 0: not available
+  uint16_t* cmax = nullptr;
+  size_t cmax_cap = 0;
+  int clog = -1;
 };
+// ensures ws->cmax holds the chunk maxima of n rows for chunks of >= 8 rows (zero padded)
+int topk_cmax_ensure(TopkWs* ws, int64_t n);
 int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg = 1);
 void topk_ws_free(TopkWs* ws);
 // scores: float32 (dtype 0) or float64 (dtype 1), n entries on device. If hist_ready, ws->hist

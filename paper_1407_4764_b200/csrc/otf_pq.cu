@@ -390,7 +390,8 @@ template <int ROWS>
 __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const uint8_t* __restrict__ codes, int64_t n,
                                                                      const double* __restrict__ lut_g, int K,
                                                                      uint16_t* __restrict__ bins_out,
-                                                                     uint32_t* __restrict__ ghist) {
+                                                                     uint32_t* __restrict__ ghist,
+                                                                     uint16_t* __restrict__ cmax) {
   extern __shared__ __align__(256) unsigned char sm[];  // [256 lines x 256 B][hist][m maxima]
   uint32_t* sh = reinterpret_cast<uint32_t*>(sm + 65536);
   uint32_t* smax = sh + kHistBins;
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
       const int64_t row = base + stride + 32 * i + lane;
       nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
     }
+    uint32_t mb = 0;  // max bin of the active rows of this lane
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       const int64_t row = base + 32 * i + lane;
@@ -500,6 +502,12 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
       }
       if (active) bins_out[row] = (uint16_t)bin;
       if (ghist) hist_add(sh, active, bin);
+      if (active) mb = max(mb, bin);
+    }
+    // the warp's 32 * ROWS consecutive rows are one top-k chunk
+    if (cmax) {
+      const uint32_t wm = __reduce_max_sync(0xffffffffu, mb);
+      if (lane == 0) cmax[base / (32 * ROWS)] = (uint16_t)wm;
     }
   }
   if (ghist) {
@@ -515,11 +523,12 @@ bool pq_fast_path(int M, const uint8_t* codes) {
 bool pq_bins_path(int M, const uint8_t* codes) { return M == 16 && pq_fast_path(M, codes); }
 
 int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
-                        uint32_t* hist, int device, cudaStream_t st) {
+                        uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax, int* clog) {
   if (n <= 0) return OTF_OK;
   static const bool f64_bins = getenv("OTF_PQ_F64_BINS") != nullptr;  // A/B switch (tools/)
   if (f64_bins) return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
   constexpr int ROWS = 4;  // 8 measured slower (128 registers, same occupancy)
+  static_assert(32 * ROWS == 128, "chunk size (clog) below");
   auto fn = pq_scan16_f32bins<ROWS>;
   static int per_sm[64] = {0};
   if (!per_sm[device & 63]) {
@@ -531,7 +540,8 @@ int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int 
   int64_t grid = (int64_t)per_sm[device & 63] * sm_count(device);
   const int64_t need = (n + kScanF32Threads * ROWS - 1) / (kScanF32Threads * ROWS);
   if (need < grid) grid = need;
-  fn<<<(int)grid, kScanF32Threads, kScanF32Smem, st>>>(codes, n, lut, K, bins, hist);
+  fn<<<(int)grid, kScanF32Threads, kScanF32Smem, st>>>(codes, n, lut, K, bins, hist, cmax);
+  if (cmax && clog) *clog = 7;  // 32 * ROWS rows per chunk
   OTF_LAUNCH_CHECK("pq_scan16_f32bins");
   return OTF_OK;
 }

@@ -28,22 +28,44 @@
 
 namespace otf {
 
+#ifdef OTF_TOPK_TRACE  // diagnostic build (tools/): per-phase globaltimer stamps of CTAs 0 and last
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TOPK_STAMP(i) \
+  if (threadIdx.x == 0) tstamp[i] = gtimer()
+#define TOPK_REPORT()                                                                                  \
+  if (threadIdx.x == 0)                                                                                \
+  printf("topk cta %d C=%lld: start %llu gend %llu hits %u maxwarp %u B %.2f gather %.2f barrier %.2f rank %.2f us\n", \
+         (int)blockIdx.x, (long long)C, (unsigned long long)(tstamp[0] % 1000000000ull),                      \
+         (unsigned long long)(tstamp[2] % 1000000000ull), s_trace[0], s_trace[1], (tstamp[1] - tstamp[0]) * 1e-3, \
+         (tstamp[2] - tstamp[1]) * 1e-3, (tstamp[3] - tstamp[2]) * 1e-3, (tstamp[4] - tstamp[3]) * 1e-3)
+#else
+#define TOPK_STAMP(i)
+#define TOPK_REPORT()
+#endif
+
 static constexpr int kTopkThreads = 1024;
 static constexpr int kTopkCtasPerSm = 1;
 static constexpr int kCandCap = 8192;                       // candidates ranked in smem
 static constexpr size_t kTopkSmem = (size_t)kCandCap * 16;  // key + inv per candidate
 
+// Grid barrier on one 64-bit word {count (low half), generation (high half)}: an arrival is one
+// atomic; the last arrival starts the next generation and zeroes the count in ONE more atomic,
+// so waiters (polling the generation) are released one L2 round trip after the last arrival.
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = bar + 1;
-    const unsigned int gen = *vgen;
+    unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    const unsigned long long old = atomicAdd(word, 1ull);
+    const unsigned int gen = (unsigned int)(old >> 32);
+    if ((unsigned int)old == nblocks - 1) {
+      atomicAdd(word, (1ull << 32) - nblocks);
     } else {
+      volatile unsigned int* vgen = bar + 1;
       while (*vgen == gen) __nanosleep(20);
     }
     __threadfence();
@@ -440,6 +462,13 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
     grid_barrier(ws.bar, nb);
   }
 
+#ifdef OTF_TOPK_TRACE
+  uint64_t tstamp[5] = {0, 0, 0, 0, 0};
+  __shared__ unsigned s_trace[2];
+  if (threadIdx.x < 2) s_trace[threadIdx.x] = 0;
+  __syncthreads();
+#endif
+  TOPK_STAMP(0);
   // ---- B: the bin holding the k-th entry ------------------------------------------------------
   int64_t C = n;
   uint32_t b0 = 0;
@@ -452,6 +481,118 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
     b0 = (uint32_t)s_b;
     C = s_above + s_cnt;
     __syncthreads();
+  }
+  TOPK_STAMP(1);
+
+  // (the plain gather below reads 8 scores per thread per pass; with fewer than ~4 passes its
+  // single round trip beats the chunk path's three)
+  if (C <= kCandCap && ws.clog >= 0 && !all && n > 32 * nthreads) {
+    // ---- C': gather through the chunk maxima ---------------------------------------------------
+    // The scoring kernel recorded the max bin of every 2^clog-row chunk; only chunks whose max
+    // reaches b0 can hold a candidate (typically ~C of n/2^clog chunks), so the gather reads the
+    // chunk maxima (2 B per chunk) plus those few chunks instead of every score.
+    const int CH = 1 << ws.clog;
+    const int64_t nch = (n + CH - 1) >> ws.clog;
+    // every warp takes a contiguous block of G chunks (hits then spread over all warps); lanes
+    // read 8 chunk maxima each (one 16-byte load) when G > 32, else one each
+    const int64_t nwarps = nthreads >> 5, wg = wbase0 >> 5;
+    int64_t G = (nch + nwarps - 1) / nwarps;
+    const bool vec = G > 32;
+    if (vec) G = (G + 7) & ~(int64_t)7;  // block starts stay 8-chunk aligned
+    const int64_t cend = min(nch, (wg + 1) * G);
+    for (int64_t cb = wg * G; cb < cend; cb += vec ? 256 : 32) {  // warp-uniform loop
+      uint32_t hits = 0;
+      if (vec) {
+        const int64_t c0 = cb + 8 * lane;  // ws.cmax has a zeroed tail past nch
+        if (c0 < cend) {
+          const uint4 q = __ldcg(reinterpret_cast<const uint4*>(ws.cmax + c0));
+          const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (c0 + e < cend && ((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu) >= b0) hits |= 1u << e;
+        }
+      } else if (cb + lane < cend && __ldcg(ws.cmax + cb + lane) >= b0) {
+        hits = 1u;
+      }
+      // the warp's hit chunks (offsets from cb) go to a per-warp list in the dynamic shared
+      // memory (free until rank_emit), then are scanned KB at a time
+      const unsigned nh = __popc(hits);
+      unsigned pos = nh;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, pos, o);
+        if (lane >= o) pos += u;
+      }
+      const unsigned H = __shfl_sync(0xffffffffu, pos, 31);
+#ifdef OTF_TOPK_TRACE
+      if (lane == 0) { atomicAdd(&s_trace[0], H); atomicMax(&s_trace[1], H); }
+#endif
+      if (H == 0u) continue;
+      uint16_t* list = reinterpret_cast<uint16_t*>(dyn) + (threadIdx.x >> 5) * 256;
+      pos -= nh;
+      for (uint32_t b = hits; b; b &= b - 1) list[pos++] = (uint16_t)(vec ? 8 * lane + __ffs(b) - 1 : lane);
+      __syncwarp();
+      constexpr int KB = 2, RPL = 4;  // chunks per batch, rows per lane per chunk (<= 128 rows)
+      using V = decltype(src.load(0));
+      for (unsigned h = 0; h < H; h += KB) {
+        V v[KB][RPL];
+        int64_t r0[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          r0[j] = h + j < H ? (cb + list[h + j]) << ws.clog : n;  // n: empty slot
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            const int64_t i = r0[j] + 32 * q + lane;
+            v[j][q] = 32 * q + lane < CH && i < n ? src.load(i) : V(0);
+          }
+        }
+        uint32_t take = 0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q)
+            if (32 * q + lane < CH && r0[j] + 32 * q + lane < n && src.bin_of(v[j][q]) >= b0)
+              take |= 1u << (j * RPL + q);
+        // one atomic for the batch, then each lane scores and stores its own candidates
+        const unsigned cnt = __popc(take);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0u) continue;
+        unsigned slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(ws.count, total);
+        int64_t slot = (int64_t)__shfl_sync(0xffffffffu, slot0, 0) + incl - cnt;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q)
+            if ((take >> (j * RPL + q)) & 1u) {
+              const int64_t i = r0[j] + 32 * q + lane;
+              if (slot < C) {
+                ws.key[slot] = score_key(src.exact(i, v[j][q]));
+                ws.inv[slot] = ~(uint64_t)id_of(ids, id_base, i);
+                ws.row[slot] = i;
+              }
+              ++slot;
+            }
+      }
+      __syncwarp();
+    }
+    TOPK_STAMP(2);
+    grid_barrier(ws.bar, nb);
+    TOPK_STAMP(3);
+    if (vb == 0) {  // every CTA has read hist and count is no longer needed
+      for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
+      if (threadIdx.x == 0) *ws.count = 0u;
+    }
+    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+    TOPK_STAMP(4);
+    TOPK_REPORT();
+    return;
   }
 
   if (C <= kCandCap) {
@@ -495,12 +636,16 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
         }
       }
     }
+    TOPK_STAMP(2);
     grid_barrier(ws.bar, nb);
+    TOPK_STAMP(3);
     if (vb == 0) {  // every CTA has read hist and count is no longer needed
       for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
     rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+    TOPK_STAMP(4);
+    TOPK_REPORT();
     return;
   }
 
@@ -544,8 +689,22 @@ int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg) {
   return OTF_OK;
 }
 
+int topk_cmax_ensure(TopkWs* ws, int64_t n) {
+  // chunks of >= 8 rows, plus a zeroed tail so the 8-chunk vector loads stay in bounds
+  const size_t need = (size_t)((n + 7) / 8) + 256;
+  if (need > ws->cmax_cap) {
+    cudaFree(ws->cmax);
+    ws->cmax = nullptr;
+    ws->cmax_cap = 0;
+    OTF_CUDA(cudaMalloc(&ws->cmax, need * sizeof(uint16_t)));
+    OTF_CUDA(cudaMemset(ws->cmax, 0, need * sizeof(uint16_t)));
+    ws->cmax_cap = need;
+  }
+  return OTF_OK;
+}
+
 void topk_ws_free(TopkWs* ws) {
-  cudaFree(ws->hist); cudaFree(ws->key); cudaFree(ws->inv); cudaFree(ws->row);
+  cudaFree(ws->hist); cudaFree(ws->key); cudaFree(ws->inv); cudaFree(ws->row); cudaFree(ws->cmax);
   *ws = TopkWs{};
 }
 

@@ -227,6 +227,38 @@ def test_pq_bit_exact(otf, golden, name):
     assert repo.payload_bytes() == codes.size and repo.model_dim == w.size
 
 
+@pytest.mark.parametrize("kind", ["edges", "ties", "tiny", "mixed"])
+def test_pq_rank_screening_paths(otf, kind):
+    """The M=16 rank scan screens in float32 and rescoring in float64 only where the float32
+    interval straddles a bin edge (otf_pq.cu pq_scan16_f32bins). Force that path: LUT entries
+    that are small dyadic numbers put every score exactly on a bin edge; heavy ties; tiny
+    (float32-subnormal) entries; a mixture of magnitudes. Ranked ids/scores must equal the
+    oracle's top_k of the reference float64 scores bit for bit."""
+    rng = np.random.default_rng({"edges": 1, "ties": 2, "tiny": 3, "mixed": 4}[kind])
+    n, k = 30_000, 500
+    if kind == "edges":
+        cents = (rng.integers(-8, 9, (16, 256, 8)) / 8.0).astype(np.float32)
+        w = np.zeros(128)
+        w[::8] = 1.0  # LUT[m][j] = c[m, j, 0]: multiples of 1/8, sums land on bin edges
+    elif kind == "ties":
+        cents = np.repeat(rng.standard_normal((16, 4, 8)), 64, axis=1).astype(np.float32)
+        w = rng.standard_normal(128)
+    elif kind == "tiny":
+        cents = (rng.standard_normal((16, 256, 8)) * 1e-30).astype(np.float32)
+        w = rng.standard_normal(128) * 1e-15
+    else:
+        cents = (rng.standard_normal((16, 256, 8)) * 10.0 ** rng.integers(-6, 6, (16, 1, 1))).astype(np.float32)
+        w = rng.standard_normal(128)
+    codes = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    ref = O.score_pq(w, cents, codes)
+    repo = otf.Repository.quantized(otf.PQCodebook(cents), codes)
+    assert repo.score(w).tobytes() == ref.tobytes()
+    r = repo.rank(otf.LinearModel(w, 1, 1), k)
+    o_ids, o_sc, _ = O.top_k(ref, k)
+    np.testing.assert_array_equal(r.ids, o_ids)
+    assert r.scores.tobytes() == np.asarray(o_sc, np.float64).tobytes()
+
+
 def test_pq_errors(otf):
     cents = np.random.default_rng(0).standard_normal((4, 8, 2)).astype(np.float32)
     book = otf.PQCodebook(cents)
