@@ -266,6 +266,17 @@ static int launch_fast(const uint8_t* codes, int64_t n, const float* cents, cons
 // is conflict-free (2 wavefronts per warp, the minimum), ~4x fewer than random bank pairs.
 // The sum is still bit-identical to pq.py:275.
 __device__ __forceinline__ uint32_t sel_u32(bool c, uint32_t a, uint32_t b) { return c ? a : b; }
+// packed float32 pairs (sm_100 FADD2): x in the low half, y in the high half
+__device__ __forceinline__ uint64_t pack_f2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 template <int ROWS>
 __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__ codes, int64_t n,
@@ -466,11 +477,11 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
       const int64_t row = base + stride + 32 * i + lane;
       nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
     }
-    uint32_t mb = 0;  // max bin of the active rows of this lane
+    // 1) screening scores of all ROWS rows (branch-free, so the rows' lookup chains interleave)
+    float s32[ROWS];
+    uint32_t need_exact = 0;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
-      const int64_t row = base + 32 * i + lane;
-      const bool active = row < n;
       // word t>>2 of the permuted row = word (t>>2) ^ (s>>2) of the code row
       const uint32_t x0 = u[i].x, x1 = u[i].y, x2 = u[i].z, x3 = u[i].w;
       const uint32_t t0 = sel_u32(s & 8, x2, x0), t1 = sel_u32(s & 8, x3, x1);
@@ -481,28 +492,66 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
 #pragma unroll
       for (int t = 0; t < 16; ++t)
         b[t] = *reinterpret_cast<const float*>(sm + __byte_perm(wd[t >> 2], kw[t >> 1], sel[t & 3]));
-      float r[8];
+      // depth-4 float32 tree on packed pairs (FADD2): P_k = (b_2k, b_2k+1); Q_k = P_k + P_k+4;
+      // R_k = Q_k + Q_k+2; S = R_0 + R_1; s32 = S.x + S.y (any fixed depth-4 tree fits eps)
+      uint64_t P[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) r[t] = __fadd_rn(b[t], b[t + 8]);
-      const float s32 = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                                  __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-      uint32_t bin = hist_bin(__fsub_rd(s32, eps));
-      const bool exact = !screen || bin != hist_bin(__fadd_ru(s32, eps));
-      if (exact) {  // rare: the exact float64 score decides the bin (numpy's pairwise order)
-        const uint32_t xw[4] = {x0, x1, x2, x3};
-        double a[16];
+      for (int k = 0; k < 8; ++k) P[k] = pack_f2(b[2 * k], b[2 * k + 1]);
 #pragma unroll
-        for (int m = 0; m < 16; ++m)
-          a[m] = *reinterpret_cast<const double*>(sm + (((xw[m >> 2] >> (8 * (m & 3))) & 0xffu) << 8) + 8 * m);
-        double rr[8];
+      for (int k = 0; k < 4; ++k) P[k] = fadd2(P[k], P[k + 4]);
+      P[0] = fadd2(P[0], P[2]);
+      P[1] = fadd2(P[1], P[3]);
+      P[0] = fadd2(P[0], P[1]);
+      // + 0.0f turns -0.0 into +0.0 (they share a bin, score_key)
+      s32[i] = __fadd_rn(__fadd_rn(__uint_as_float((uint32_t)P[0]), __uint_as_float((uint32_t)(P[0] >> 32))), 0.0f);
+      // [lo, hi] inside one bin <=> their order keys agree in the top 12 bits <=> their bit
+      // patterns do (same sign; -0.0 vs +0.0 counts as different: conservative)
+      const float lo = __fsub_rd(s32[i], eps), hi = __fadd_ru(s32[i], eps);
+      if (!screen || (__float_as_uint(lo) ^ __float_as_uint(hi)) >= (1u << 20)) need_exact |= 1u << i;
+    }
+    uint32_t bin[ROWS];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
-        bin = hist_bin(__dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
-                                 __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7]))));
+    for (int i = 0; i < ROWS; ++i) {  // order key of a float without the -0.0 test (done above)
+      const uint32_t v = __float_as_uint(s32[i]);
+      bin[i] = (v ^ ((uint32_t)((int32_t)v >> 31) | 0x80000000u)) >> 20;
+    }
+    // 2) rare: rows whose interval straddles a bin edge take the exact float64 score (numpy's
+    //    pairwise order) and its bin
+    if (need_exact) {
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) {
+        if ((need_exact >> i) & 1u) {
+          const uint32_t xw[4] = {u[i].x, u[i].y, u[i].z, u[i].w};
+          double a[16];
+#pragma unroll
+          for (int m = 0; m < 16; ++m)
+            a[m] = *reinterpret_cast<const double*>(sm + (((xw[m >> 2] >> (8 * (m & 3))) & 0xffu) << 8) + 8 * m);
+          double rr[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
+          bin[i] = hist_bin(__dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                                      __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7]))));
+        }
       }
-      if (active) bins_out[row] = (uint16_t)bin;
-      if (ghist) hist_add(sh, active, bin);
-      if (active) mb = max(mb, bin);
+    }
+    // 3) bins, histogram, chunk maximum
+    uint32_t mb = 0;  // max bin of the active rows of this lane
+    if (base + 32 * ROWS <= n) {  // full batch (all but the last): no per-row bounds checks
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) {
+        bins_out[base + 32 * i + lane] = (uint16_t)bin[i];
+        if (ghist) hist_add(sh, true, bin[i]);
+        mb = max(mb, bin[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) {
+        const int64_t row = base + 32 * i + lane;
+        const bool active = row < n;
+        if (active) bins_out[row] = (uint16_t)bin[i];
+        if (ghist) hist_add(sh, active, bin[i]);
+        if (active) mb = max(mb, bin[i]);
+      }
     }
     // the warp's 32 * ROWS consecutive rows are one top-k chunk
     if (cmax) {
@@ -527,8 +576,9 @@ int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int 
   if (n <= 0) return OTF_OK;
   static const bool f64_bins = getenv("OTF_PQ_F64_BINS") != nullptr;  // A/B switch (tools/)
   if (f64_bins) return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
-  constexpr int ROWS = 4;  // 8 measured slower (128 registers, same occupancy)
-  static_assert(32 * ROWS == 128, "chunk size (clog) below");
+  // 4 rows per thread (software-pipelined, ~112 registers, one 512-thread CTA per SM); 2 rows at
+  // 64 registers (two CTAs per SM) rematerialises the per-lane constants and ran 33% slower
+  constexpr int ROWS = 4;
   auto fn = pq_scan16_f32bins<ROWS>;
   static int per_sm[64] = {0};
   if (!per_sm[device & 63]) {
