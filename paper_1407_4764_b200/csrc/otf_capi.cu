@@ -119,6 +119,8 @@ struct otf_repo {
   HostBuf h_w, h_out;
   TopkWs topk;
   TopkWs mtopk;  // segment workspace of rank_many (kept apart: graphs capture topk's pointers)
+  bool x_exp_ready = false;  // the FP16 data scale of score_many (dense payload is immutable)
+  int x_exp = 0;
   // graph cache for otf_repo_rank_graph
   cudaGraphExec_t gexec = nullptr;
   const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -309,7 +311,7 @@ int64_t otf_launch_count(void) { return g_launches.load(); }
 const char* otf_kernel_names(void) {
   return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;pq_scan16_xor;"
          "pq_scan_generic;pq_scan16_f32bins;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
-         "bin_hamming;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
+         "bin_hamming;split_w_half_kernel;absmax_kernel;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
          "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local";
 }
 
@@ -515,8 +517,14 @@ int stage_many(otf_repo* r, const double* W, int n_cls, cudaStream_t st, const d
 int multi_score_group(otf_repo* r, const double* dW, int cn, float* out, cudaStream_t st) {
   int rc = r->w32.ensure((size_t)multi_ws_floats(r->model_dim) * sizeof(float));
   if (rc) return rc;
+  if (!r->x_exp_ready) {  // one pass over the repository, on the first multi-classifier call
+    if ((rc = multi_x_exponent(static_cast<const float*>(r->payload), r->n, r->model_dim, r->device, st,
+                               &r->x_exp)))
+      return rc;
+    r->x_exp_ready = true;
+  }
   return launch_multi_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dW, cn,
-                            static_cast<float*>(r->w32.p), out, r->device, st);
+                            static_cast<float*>(r->w32.p), out, r->device, st, r->x_exp);
 }
 }  // namespace
 

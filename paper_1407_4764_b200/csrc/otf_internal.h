@@ -128,7 +128,11 @@ namespace otf {
 // many classifiers (otf_multi.cu): tcgen05 TF32x3 scoring, out (n_cls x n float32)
 bool multi_tc_supported(int d, const float* X);
 // float32 scratch launch_multi_score needs for the split, pre-tiled classifier matrix
-inline size_t multi_ws_floats(int d) { return (size_t)3 * 64 * (size_t)d; }
+inline size_t multi_ws_floats(int d) { return (size_t)3 * 64 * (size_t)d + 64; }
+// x_exp: the data scale exponent from multi_x_exponent (INT_MIN: TF32x3 form), see otf_multi.cu
 int launch_multi_score(const float* X, int64_t n, int d, const double* W, int n_cls, float* ws, float* out,
-                       int device, cudaStream_t st);
+                       int device, cudaStream_t st, int x_exp);
+// one pass over X (synchronises st): ex with max|x| 2^ex in [2^14, 2^15), or INT_MIN if X holds
+// inf/NaN or an extreme magnitude
+int multi_x_exponent(const float* X, int64_t n, int d, int device, cudaStream_t st, int* ex);
 }  // namespace otf

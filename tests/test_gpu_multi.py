@@ -1,9 +1,11 @@
 """Many classifiers at once (C5b) on the tcgen05 tensor cores, through the C ABI.
 
 Bar: every classifier's scores stay within the reference tolerance of its own score_dense
-(ranker.py:63-69; 1e-6 * ||w|| * ||x||) and within the documented error of the TF32x3 split of
-the exact dot; rank_many equals the oracle's exact top_k of those scores; a row's scores do not
-depend on its position (128-row tiles, padding rows, permutations).
+(ranker.py:63-69; 1e-6 * ||w|| * ||x||) and within the documented error of the split products
+of the exact dot (FP16 form, the default: x1 w1 + x1 w2 + x2 w1 in kind::f16; TF32 form:
+x_hi w_hi + x_hi w_lo + x_lo w_hi in kind::tf32 — both <= 2^-20 of sum |x_j w_j| with the
+float32 accumulation); rank_many equals the oracle's exact top_k of those scores; a row's scores
+do not depend on its position (128-row tiles, padding rows, permutations).
 """
 
 import numpy as np
@@ -18,8 +20,18 @@ def exact(x, W):
     return x.astype(np.float64) @ W.astype(np.float32).astype(np.float64).T
 
 
+@pytest.fixture(params=["fp16", "tf32"])
+def form(request, monkeypatch):
+    """Both operand forms of otf_multi.cu (OTF_MULTI_TF32=1 selects the TF32x3 kernel)."""
+    if request.param == "tf32":
+        monkeypatch.setenv("OTF_MULTI_TF32", "1")
+    else:
+        monkeypatch.delenv("OTF_MULTI_TF32", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("n,d,c", [(1000, 128, 7), (129, 32, 1), (4096, 256, 64), (777, 4096, 3), (300, 2048, 70)])
-def test_score_many_matches_dense(otf, n, d, c):
+def test_score_many_matches_dense(otf, form, n, d, c):
     rng = np.random.default_rng(n + d + c)
     x = rng.standard_normal((n, d)).astype(np.float32)
     x /= np.linalg.norm(x, axis=1, keepdims=True)
@@ -29,9 +41,9 @@ def test_score_many_matches_dense(otf, n, d, c):
     assert S.shape == (c, n) and S.dtype == np.float32
     ex = exact(x, W).T
     mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
-    # TF32 x3: dropped lo*lo and TF32 truncation of the lo parts (<= 2^-21 relative per product),
-    # float32 accumulation restarted every 128 K values (measured max 2^-22 of mag, numpy's own
-    # float32 sgemm: 2^-22.3) -> a 4x margin
+    # TF32 x3: dropped lo*lo and TF32 truncation of the lo parts (<= 2^-21 relative per product);
+    # FP16: dropped x2*w2 and the float16 rounding of x2, w2 (<= 3 * 2^-22); float32 accumulation
+    # restarted every 128 K values (measured max 2^-22 of mag, numpy's own float32 sgemm: 2^-22.3)
     assert np.all(np.abs(S - ex) <= 2.0 ** -20 * mag + np.spacing(np.abs(S)) + 1e-30)
     for i in range(min(c, 5)):
         ref = O.score_dense(W[i], x)
@@ -65,6 +77,33 @@ def test_rank_many_exact_topk(otf):
         assert lists[i].model_version == 3
 
 
+@pytest.mark.parametrize("case", ["huge", "tiny", "inf_row", "classifier_range"])
+def test_score_many_data_scales(otf, case):
+    """The FP16 form scales X by 2^ex (max |x| 2^ex in [2^14, 2^15), one pass per repository) and
+    each classifier by its own 2^ew; extreme data magnitudes and non-finite data use the TF32 form.
+    Finite rows stay within the bound either way."""
+    rng = np.random.default_rng({"huge": 1, "tiny": 2, "inf_row": 3, "classifier_range": 4}[case])
+    n, d, c = 700, 256, 9
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    W = rng.standard_normal((c, d))
+    if case == "huge":
+        x *= np.float32(1e12)
+    elif case == "tiny":
+        x *= np.float32(1e-25)  # 2^ex out of the FP16 form's range -> TF32 form
+    elif case == "inf_row":
+        x[17, 3] = np.inf
+    else:
+        W *= 10.0 ** np.arange(-12, 15, 3)[:, None]
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    S = repo.score_many(list(W))
+    ok = np.isfinite(x).all(axis=1)
+    ex = exact(x[ok], W).T
+    mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x[ok].astype(np.float64)).T
+    assert np.all(np.abs(S[:, ok] - ex) <= 2.0 ** -20 * mag + np.spacing(np.abs(S[:, ok])) + 1e-30)
+    if case == "inf_row":
+        assert not np.all(np.isfinite(S[:, 17]))
+
+
 def test_multi_errors(otf):
     repo = otf.Repository.dense(otf.FeatureStore(np.ones((10, 30), np.float32)))
     with pytest.raises(otf.ConfigError):
@@ -75,7 +114,7 @@ def test_multi_errors(otf):
 
 
 @pytest.mark.parametrize("n,d,c", [(1000, 128, 7), (300, 2048, 64)])
-def test_single_cta_path_matches_pair_path(otf, monkeypatch, n, d, c):
+def test_single_cta_path_matches_pair_path(otf, monkeypatch, form, n, d, c):
     """The CTA-pair kernel (default) and the single-CTA kernel (inputs of one 128-row tile, forced
     here with OTF_MULTI_SINGLE) both meet the TF32x3 bound and agree with each other."""
     rng = np.random.default_rng(n * 7 + c)
