@@ -107,13 +107,21 @@ int otf_repo_rank(otf_repo* repo, const double* w, int64_t k, int64_t* out_ids,
 
 /* Many classifiers over one dense repository (C5b; no single reference call — the reference
  * needs n_cls separate score_dense calls, ranker.py:63-69). W: (n_cls, model_dim) float64.
- * Scores on the tcgen05 tensor cores in TF32 with a 3-product split (float32-level accuracy);
+ * Scores on the tcgen05 tensor cores with 3 split products (float32-level accuracy): FP16
+ * (kind::f16) by default, TF32 for data holding inf/NaN or extreme magnitudes;
  * requires model_dim % 32 == 0. out: (n_cls, count) float32, classifier-major. */
 int otf_repo_score_many(otf_repo* repo, const double* W, int32_t n_cls, float* out, int mem,
                         void* stream);
 /* ... and the exact top-k of each classifier: out_ids / out_scores (n_cls, n_out). */
 int otf_repo_rank_many(otf_repo* repo, const double* W, int32_t n_cls, int64_t k, int64_t* out_ids,
                        double* out_scores, int64_t* out_n, int mem, void* stream);
+
+/* Measurement hook (no reference counterpart; used by bench.py for the roofline): runs the
+ * scoring kernel of otf_repo_rank exactly as rank does (PQ: the float32-screening bins scan; with
+ * the fused histogram and chunk maxima) for a device-resident w on `stream`, times that kernel
+ * with CUDA events recorded around its launch(es) on the same stream, and returns the elapsed
+ * milliseconds in *ms (synchronises the stream; leaves the rank workspace clean). */
+int otf_repo_time_rank_scan(otf_repo* repo, const double* w_dev, float* ms, void* stream);
 
 /* Capture repo's rank(k) for a device-resident w into a CUDA graph and replay it
  * (the live ranker re-ranks every tau with a new w in the same buffer). Device memory only. */

@@ -471,6 +471,42 @@ int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* strea
   return OTF_OK;
 }
 
+int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* stream) {
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  if (!ms) return fail(OTF_ERR_CONFIG, "ms must not be NULL");
+  cudaStream_t st = pick_stream(r->stream, stream);
+  const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+  int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
+  if (!rc) rc = topk_ws_alloc(&r->topk, 1);
+  if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
+  const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
+  const bool bins = r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes);
+  if (!rc && bins) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t));
+  if (!rc && bins) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
+  if (!rc && bins) rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  OTF_CUDA(cudaEventCreate(&e0));
+  OTF_CUDA(cudaEventCreate(&e1));
+  int clog = -1;
+  cudaEventRecord(e0, st);
+  if (bins)
+    rc = launch_pq_scan_bins(codes, r->n, static_cast<const double*>(r->lut.p), r->K,
+                             static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st, r->topk.cmax, &clog);
+  else
+    rc = score_into(r, w_dev, r->scores.p, r->topk.hist, st, r->topk.cmax, &clog);
+  cudaEventRecord(e1, st);
+  if (!rc) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBins * sizeof(uint32_t), st) == cudaSuccess
+                    ? OTF_OK : cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
+  cudaError_t e = cudaEventSynchronize(e1);
+  if (!rc && e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (!rc && e != cudaSuccess) rc = cuda_fail(e, "otf_repo_time_rank_scan");
+  return rc;
+}
+
 int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, double* out_scores,
                   int64_t* out_rows, int64_t* out_n, int mem, void* stream) {
   std::lock_guard<std::mutex> lk(r->mu);
