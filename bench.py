@@ -412,9 +412,16 @@ def run_gpu(args, cfg):
         o_rows = torch.empty(k, dtype=torch.int64, device=dev)
         got = C.c_int64()
 
-        def step():
-            _lib.check(lib.otf_repo_rank(repo.handle, _lib.tptr(w_dev), k, _lib.tptr(o_ids), _lib.tptr(o_sc),
-                                         _lib.tptr(o_rows), C.byref(got), _lib.MEM_DEVICE, sp))
+        if os.environ.get("OTF_BENCH_NO_GRAPH"):
+            def step():
+                _lib.check(lib.otf_repo_rank(repo.handle, _lib.tptr(w_dev), k, _lib.tptr(o_ids), _lib.tptr(o_sc),
+                                             _lib.tptr(o_rows), C.byref(got), _lib.MEM_DEVICE, sp))
+        else:
+            # the live ranker's path (session.rank_tick): the query's kernels replayed from the
+            # repository's cached CUDA graph (no per-launch host work between the kernels)
+            def step():
+                _lib.check(lib.otf_repo_rank_graph(repo.handle, _lib.tptr(w_dev), k, _lib.tptr(o_ids),
+                                                   _lib.tptr(o_sc), _lib.tptr(o_rows), sp))
 
     payload = n_local * row_bytes(cfg)
     flush = payload < 4 * L2_BYTES

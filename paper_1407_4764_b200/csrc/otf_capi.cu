@@ -125,6 +125,7 @@ struct otf_repo {
   cudaGraphExec_t gexec = nullptr;
   const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int64_t g_k = -1;
+  int g_kernels = 0;  // kernels in the captured graph (launch accounting of each replay)
 };
 
 struct otf_trainer {
@@ -665,7 +666,10 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     cudaStream_t cap;
     OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     OTF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = g_launches.load();
     rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
+    r->g_kernels = (int)(g_launches.load() - l0);
+    g_launches.fetch_sub(r->g_kernels);  // captured, not launched
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
     cudaStreamDestroy(cap);
@@ -678,7 +682,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     r->g_k = k_eff;
   }
   OTF_CUDA(cudaGraphLaunch(r->gexec, st));
-  count_launch(3);
+  count_launch(r->g_kernels);
   return OTF_OK;
 }
 }  // namespace
