@@ -64,8 +64,9 @@ int64_t otf_launch_count(void);
 typedef struct otf_repo otf_repo;
 
 /* Repository.dense(store) — ranker.py:176-178. data is (n, dim) float32 row-major.
- * ids: n int64 (NULL = id_base + row). If mem == OTF_MEM_DEVICE and borrow != 0 the handle
- * reads `data` in place (caller keeps it alive); otherwise it copies into its own HBM. */
+ * ids: n int64 (NULL = id_base + row), in host or device memory (detected from the pointer,
+ * independently of mem). If mem == OTF_MEM_DEVICE and borrow != 0 the handle reads `data` in
+ * place (caller keeps it alive); otherwise it copies into its own HBM. */
 int otf_repo_create_dense(int device, const float* data, int64_t n, int32_t dim,
                           const int64_t* ids, int64_t id_base, int mem, int borrow,
                           otf_repo** out);

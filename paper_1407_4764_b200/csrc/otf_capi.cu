@@ -178,10 +178,17 @@ int repo_common(otf_repo* r, int device, int64_t n, const int64_t* ids, int64_t 
   int rc = make_stream(&r->stream, false);
   if (rc) return rc;
   if (ids) {
-    rc = check_ids(ids, n, mem);
+    // ids may be host or device memory whatever `mem` says of the payload (from_device adopts a
+    // device payload with host ids): the pointer decides
+    cudaPointerAttributes pa;
+    const bool dev_ids = cudaPointerGetAttributes(&pa, ids) == cudaSuccess &&
+                         (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();  // clear a failed query
+    const int ids_mem = dev_ids ? OTF_MEM_DEVICE : OTF_MEM_HOST;
+    rc = check_ids(ids, n, ids_mem);
     if (rc) return rc;
     OTF_CUDA(cudaMalloc(&r->ids, (size_t)(n > 0 ? n : 1) * sizeof(int64_t)));
-    rc = copy_in(r->ids, ids, (size_t)n * sizeof(int64_t), mem, r->stream);
+    rc = copy_in(r->ids, ids, (size_t)n * sizeof(int64_t), ids_mem, r->stream);
     if (rc) return rc;
   }
   return OTF_OK;
