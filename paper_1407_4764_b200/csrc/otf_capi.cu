@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -897,6 +898,28 @@ int otf_hamming(int device, const uint8_t* a, const uint8_t* b, int64_t n, int32
   return S.out(out, dout, (size_t)n * 8, mem);
 }
 
+namespace {
+struct CachedTopkWs {
+  TopkWs ws;
+  cudaEvent_t done = nullptr;
+  int device = 0;
+  ~CachedTopkWs() {
+    if (done) {
+      cudaSetDevice(device);
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+    }
+    topk_ws_free(&ws);
+  }
+};
+CachedTopkWs& cached_topk_ws(int device) {
+  static thread_local std::map<int, CachedTopkWs> per_device;
+  CachedTopkWs& c = per_device[device];
+  c.device = device;
+  return c;
+}
+}  // namespace
+
 int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const int64_t* ids, int64_t k,
               int64_t* out_ids, double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
               void* stream) {
@@ -907,7 +930,14 @@ int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const in
   const size_t es = dtype == OTF_F64 ? 8 : 4;
   const void *ds, *di = nullptr;
   void *d_ids, *d_sc, *d_rows = nullptr;
-  TopkWs ws;
+  // the calling thread's cached workspace for this device (the multi-GPU merge calls this once
+  // per query: no allocation, no host synchronisation in device mode); a call waits for the
+  // previous call's kernel before reusing it, whatever stream that ran on
+  CachedTopkWs& cw = cached_topk_ws(device);
+  TopkWs& ws = cw.ws;
+  if (cw.done && (rc = cudaStreamWaitEvent(st, cw.done, 0) == cudaSuccess ? OTF_OK
+                                                                      : cuda_fail(cudaGetLastError(), "wait")))
+    return rc;
   if ((rc = S.in(scores, (size_t)n * es, mem, &ds))) return rc;
   if (ids && (rc = S.in(ids, (size_t)n * 8, mem, &di))) return rc;
   if ((rc = S.outbuf(out_ids, (size_t)k_eff * 8, mem, &d_ids))) return rc;
@@ -916,11 +946,15 @@ int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const in
   rc = launch_topk(ds, dtype, n, static_cast<const int64_t*>(di), 0, k_eff, &ws, false,
                    static_cast<int64_t*>(d_ids), static_cast<double*>(d_sc),
                    static_cast<int64_t*>(d_rows), device, st);
+  if (!rc) {
+    if (!cw.done) rc = cudaEventCreateWithFlags(&cw.done, cudaEventDisableTiming) == cudaSuccess
+                           ? OTF_OK : cuda_fail(cudaGetLastError(), "cudaEventCreate");
+    if (!rc) cudaEventRecord(cw.done, st);
+  }
   if (!rc) rc = S.out(out_ids, d_ids, (size_t)k_eff * 8, mem);
   if (!rc) rc = S.out(out_scores, d_sc, (size_t)k_eff * 8, mem);
   if (!rc && out_rows) rc = S.out(out_rows, d_rows, (size_t)k_eff * 8, mem);
-  cudaStreamSynchronize(st);
-  topk_ws_free(&ws);
+  if (rc) cudaStreamSynchronize(st);
   return rc;
 }
 
