@@ -123,10 +123,18 @@ struct otf_repo {
   bool x_exp_ready = false;  // the FP16 data scale of score_many (dense payload is immutable)
   int x_exp = 0;
   // graph cache for otf_repo_rank_graph
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  int64_t g_k = -1;
-  int g_kernels = 0;  // kernels in the captured graph (launch accounting of each replay)
+  // cached CUDA graphs of rank (otf_repo_rank_graph and host-memory otf_repo_rank): keyed by k
+  // and EVERY pointer a replay touches (w, outputs, stream and the handle's workspaces), so a
+  // workspace that grew (e.g. a larger k) can never be replayed through a stale graph
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[13] = {};
+    int64_t k = -1;
+    int kernels = 0;  // kernels in the graph (launch accounting of each replay)
+    uint64_t used = 0;
+  };
+  std::vector<GraphEntry> graphs;  // <= kGraphCache entries, least recently used replaced
+  uint64_t graph_clock = 0;
 };
 
 struct otf_trainer {
@@ -212,7 +220,8 @@ void repo_free(otf_repo* r) {
   if (!r) return;
   DeviceGuard g(r->device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  for (auto& ge : r->graphs)
+    if (ge.exec) cudaGraphExecDestroy(ge.exec);
   if (r->owns_payload && r->payload) cudaFree(const_cast<void*>(r->payload));
   if (r->ids) cudaFree(r->ids);
   if (r->cents) cudaFree(r->cents);
@@ -516,6 +525,11 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   return rc;
 }
 
+namespace {
+int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* ids_dev, double* scores_dev,
+                      int64_t* rows_dev, cudaStream_t st);
+}  // namespace
+
 int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, double* out_scores,
                   int64_t* out_rows, int64_t* out_n, int mem, void* stream) {
   std::lock_guard<std::mutex> lk(r->mu);
@@ -534,7 +548,9 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
   int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
   double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
-  if ((rc = rank_device(r, dw, k_eff, d_ids, d_sc, d_rows, st))) return rc;
+  // host calls replay the repository's cached graph of the query (staging and output buffers
+  // are the handle's own, so the graph is reused by every host-memory rank of this k)
+  if ((rc = rank_graph_locked(r, dw, k_eff, d_ids, d_sc, d_rows, st))) return rc;
   OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
   OTF_CUDA(cudaStreamSynchronize(st));
   const int64_t* h_ids = static_cast<const int64_t*>(r->h_out.p);
@@ -656,41 +672,59 @@ namespace {
 // for a given (w, outputs, stream, k), replayed afterwards). Caller holds r->mu.
 int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* ids_dev, double* scores_dev,
                       int64_t* rows_dev, cudaStream_t st) {
-  const void* key[6] = {w_dev, ids_dev, scores_dev, rows_dev, st, nullptr};
-  bool hit = r->gexec && r->g_k == k_eff;
-  for (int i = 0; i < 5 && hit; ++i) hit = key[i] == r->g_key[i];
+  constexpr size_t kGraphCache = 4;
+  // allocate everything outside capture (no-ops once the workspaces are large enough)
+  const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+  int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
+  if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
+  if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
+  if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
+  if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
+  if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
+  if (rc) return rc;
+  const void* key[13] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
+                         r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax};
+  otf_repo::GraphEntry* hit = nullptr;
+  for (auto& ge : r->graphs) {
+    bool same = ge.exec && ge.k == k_eff;
+    for (int i = 0; i < 13 && same; ++i) same = ge.key[i] == key[i];
+    if (same) { hit = &ge; break; }
+  }
   if (!hit) {
-    if (r->gexec) { cudaGraphExecDestroy(r->gexec); r->gexec = nullptr; }
-    // allocate everything outside capture
-    const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
-    int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
-    if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
-    if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
-    if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
-    if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
-    if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
-    if (rc) return rc;
     OTF_CUDA(cudaStreamSynchronize(st));  // allocations above must not race the capture
     cudaStream_t cap;
     OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     OTF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     const int64_t l0 = g_launches.load();
     rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
-    r->g_kernels = (int)(g_launches.load() - l0);
-    g_launches.fetch_sub(r->g_kernels);  // captured, not launched
+    const int kernels = (int)(g_launches.load() - l0);
+    g_launches.fetch_sub(kernels);  // captured, not launched
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
     cudaStreamDestroy(cap);
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
-    if (e != cudaSuccess) { r->gexec = nullptr; return cuda_fail(e, "cudaGraphInstantiate"); }
-    for (int i = 0; i < 5; ++i) r->g_key[i] = key[i];
-    r->g_k = k_eff;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    if (r->graphs.size() < kGraphCache) {
+      r->graphs.emplace_back();
+      hit = &r->graphs.back();
+    } else {
+      hit = &r->graphs[0];
+      for (auto& ge : r->graphs)
+        if (ge.used < hit->used) hit = &ge;
+      cudaGraphExecDestroy(hit->exec);
+    }
+    hit->exec = exec;
+    for (int i = 0; i < 13; ++i) hit->key[i] = key[i];
+    hit->k = k_eff;
+    hit->kernels = kernels;
   }
-  OTF_CUDA(cudaGraphLaunch(r->gexec, st));
-  count_launch(r->g_kernels);
+  hit->used = ++r->graph_clock;
+  OTF_CUDA(cudaGraphLaunch(hit->exec, st));
+  count_launch(hit->kernels);
   return OTF_OK;
 }
 }  // namespace
