@@ -438,14 +438,17 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
   }
   __syncthreads();
   float eps;
+  bool screen;
   {
-    double e = 0.0;
+    double e = 0.0;  // S = sum_m max_j |LUT[m][j]| bounds every partial sum of the float32 tree
 #pragma unroll
     for (int m = 0; m < 16; ++m) e += (double)__uint_as_float(smax[m]);
-    eps = __double2float_ru(e * 0x1p-20);  // NaN/inf when the LUT is not finite
+    eps = __double2float_ru(e * 0x1p-20);
     eps = fmaxf(eps, 0x1p-140f);  // absolute floor: float32 underflow of tiny entries
+    // no float32 partial sum can overflow when S <= 1e38 (and NaN/inf LUTs fail the test):
+    // otherwise every row takes the exact path
+    screen = e <= 1.0e38;
   }
-  const bool screen = eps <= 3.0e38f;  // false: every row takes the exact path
   const int lane = threadIdx.x & 31;
   const uint32_t s = lane & 15;
   // per step pair u: K word [offset of table 2u^s, offset of table (2u+1)^s, 0, 0] (copy lane>>4)

@@ -227,14 +227,14 @@ def test_pq_bit_exact(otf, golden, name):
     assert repo.payload_bytes() == codes.size and repo.model_dim == w.size
 
 
-@pytest.mark.parametrize("kind", ["edges", "ties", "tiny", "mixed"])
+@pytest.mark.parametrize("kind", ["edges", "ties", "tiny", "mixed", "huge"])
 def test_pq_rank_screening_paths(otf, kind):
     """The M=16 rank scan screens in float32 and rescoring in float64 only where the float32
     interval straddles a bin edge (otf_pq.cu pq_scan16_f32bins). Force that path: LUT entries
     that are small dyadic numbers put every score exactly on a bin edge; heavy ties; tiny
     (float32-subnormal) entries; a mixture of magnitudes. Ranked ids/scores must equal the
     oracle's top_k of the reference float64 scores bit for bit."""
-    rng = np.random.default_rng({"edges": 1, "ties": 2, "tiny": 3, "mixed": 4}[kind])
+    rng = np.random.default_rng({"edges": 1, "ties": 2, "tiny": 3, "mixed": 4, "huge": 5}[kind])
     n, k = 30_000, 500
     if kind == "edges":
         cents = (rng.integers(-8, 9, (16, 256, 8)) / 8.0).astype(np.float32)
@@ -246,9 +246,12 @@ def test_pq_rank_screening_paths(otf, kind):
     elif kind == "tiny":
         cents = (rng.standard_normal((16, 256, 8)) * 1e-30).astype(np.float32)
         w = rng.standard_normal(128) * 1e-15
-    else:
+    elif kind == "mixed":
         cents = (rng.standard_normal((16, 256, 8)) * 10.0 ** rng.integers(-6, 6, (16, 1, 1))).astype(np.float32)
         w = rng.standard_normal(128)
+    else:  # LUT entries near the float32 range: partial float32 sums could overflow
+        cents = (rng.standard_normal((16, 256, 8)) * 1e37).astype(np.float32)
+        w = rng.standard_normal(128) * 10.0
     codes = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     ref = O.score_pq(w, cents, codes)
     repo = otf.Repository.quantized(otf.PQCodebook(cents), codes)
