@@ -101,8 +101,15 @@ struct DirectSrc {
   const ST* s;
   __device__ __forceinline__ void shift(int64_t o) { s += o; }
   __device__ __forceinline__ ST load(int64_t i) const { return __ldcg(s + i); }
-  // 8 consecutive entries from i (i % 8 == 0): two float4 / four double2 loads.
+  // 8 consecutive entries from i (i % 8 == 0): two float4 / four double2 loads, or scalar loads
+  // when the array does not start on 16 bytes (segments at c * n entries with n % 4 != 0, or a
+  // caller's unaligned score array)
   __device__ __forceinline__ void load8(int64_t i, ST (&v)[8]) const {
+    if ((reinterpret_cast<uintptr_t>(s) & 15) != 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(s + i + q);
+      return;
+    }
     if constexpr (sizeof(ST) == 4) {
       const float4 a = __ldcg(reinterpret_cast<const float4*>(s + i));
       const float4 b = __ldcg(reinterpret_cast<const float4*>(s + i) + 1);
@@ -453,9 +460,27 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
     uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
     hist_zero(sh);
     __syncthreads();
-    for (int64_t base = wbase0; base < n; base += nthreads) {
-      const int64_t i = base + lane;
-      if (i < n) hist_add(sh, true, src.bin_of(src.load(i)));
+    // each lane reads 2 x 8 consecutive entries per pass (vector loads; 16 in flight)
+    constexpr int UA = 8, RA = 2;
+    using VA = decltype(src.load(0));
+    for (int64_t wb = wbase0 * UA * RA; wb < n; wb += nthreads * UA * RA) {  // warp-uniform loop
+      VA v[RA][UA];
+#pragma unroll
+      for (int g = 0; g < RA; ++g) {
+        const int64_t base = wb + (int64_t)(g * 32 + lane) * UA;
+        if (base + UA <= n) {
+          src.load8(base, v[g]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < UA; ++q) v[g][q] = base + q < n ? src.load(base + q) : VA(0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < RA; ++g) {
+        const int64_t base = wb + (int64_t)(g * 32 + lane) * UA;
+#pragma unroll
+        for (int q = 0; q < UA; ++q) hist_add(sh, base + q < n, src.bin_of(v[g][q]));
+      }
     }
     __syncthreads();
     hist_flush(sh, ws.hist);

@@ -155,3 +155,20 @@ def test_rank_many_segmented_topk(otf, n, d, c, k):
     # the single-classifier ranking of the same repository is unaffected (separate workspace)
     r1 = repo.rank(otf.LinearModel(W[1], 1, 1), k)
     assert len(r1.ids) == min(k, n)
+
+
+@pytest.mark.parametrize("n,c", [(1001, 3), (5003, 64), (2, 5)])
+def test_rank_many_unaligned_segments(otf, n, c):
+    """Classifier-major score rows start at c * n floats: n not a multiple of 4 leaves them
+    unaligned for the top-k's vector loads (they fall back to scalar loads)."""
+    rng = np.random.default_rng(n + c)
+    x = rng.standard_normal((n, 64)).astype(np.float32)
+    W = rng.standard_normal((c, 64))
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    S = repo.score_many(list(W))
+    k = min(n, 50)
+    lists = repo.rank_many([otf.LinearModel(w, 1, 1) for w in W], k)
+    for i in range(c):
+        o_ids, o_sc, _ = O.top_k(S[i], k)
+        np.testing.assert_array_equal(lists[i].ids, o_ids)
+        np.testing.assert_array_equal(lists[i].scores, o_sc)
