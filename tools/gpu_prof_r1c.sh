@@ -1,0 +1,12 @@
+# Refresh profiles/ (round 1, third pass): per config a plain bench line, the ncu launch list and
+# one --set full capture of the rank path's scoring kernel (+ top-k).
+mkdir -p gpurun_out
+for spec in "c2:dense_score|topk:2" "c1:dense_score|topk:2" "c3:pq_scan16_f32bins|topk:2" "c5a:bin_score|topk:3" \
+            "c5b:multi_score|topk:2" ; do
+  IFS=: read cfg kr cnt <<< "$spec"
+  timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu > gpurun_out/r1c_plain_$cfg.log 2>&1; echo plain_$cfg=$?
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1c_$cfg.csv \
+      python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu > /dev/null 2>&1; echo launches_$cfg=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kr" -s 4 -c $cnt -o gpurun_out/prof_r1c_$cfg \
+      python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu > /dev/null 2>&1; echo full_$cfg=$?
+done

@@ -63,15 +63,10 @@ def main(rep, out):
     if score:
         summary["dram_bytes_per_launch"] = score[0].get("dram_bytes_total")
         summary["score_kernel"] = score[0]["kernel"]
-        # the binary scan is one launch per 128-byte slice: one scoring call = the consecutive
-        # slice launches (capture them together with -c <slices>)
+        # the binary scan is one launch per 128-byte slice: one scoring call = one launch of each
+        # slice (capture -c <slices + 1> so each slice appears once, in any order)
         if "bin_score_bytes" in score[0]["kernel"]:
-            i0 = launches.index(score[0])
-            run = [score[0]]
-            for l in launches[i0 + 1:]:
-                if "bin_score_bytes" not in l["kernel"]:
-                    break
-                run.append(l)
+            run = [l for l in launches if "bin_score_bytes" in l["kernel"]]
             summary["dram_bytes_per_launch"] = sum(l.get("dram_bytes_total", 0.0) for l in run)
             summary["score_launches_summed"] = len(run)
     with open(out, "w") as f:
