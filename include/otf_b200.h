@@ -110,7 +110,10 @@ int otf_repo_rank(otf_repo* repo, const double* w, int64_t k, int64_t* out_ids,
  * needs n_cls separate score_dense calls, ranker.py:63-69). W: (n_cls, model_dim) float64.
  * Scores on the tcgen05 tensor cores with 3 split products (float32-level accuracy): FP16
  * (kind::f16) by default, TF32 for data holding inf/NaN or extreme magnitudes;
- * requires model_dim % 32 == 0. out: (n_cls, count) float32, classifier-major. */
+ * requires model_dim % 32 == 0. out: (n_cls, count) float32, classifier-major.
+ * The FP16 form scales the data by a power of two derived from max |x| in ONE pass on the first
+ * call (cached in the handle): the payload must not change afterwards (a borrowed buffer that is
+ * rewritten needs a new handle). */
 int otf_repo_score_many(otf_repo* repo, const double* W, int32_t n_cls, float* out, int mem,
                         void* stream);
 /* ... and the exact top-k of each classifier: out_ids / out_scores (n_cls, n_out). */
