@@ -328,7 +328,7 @@ int64_t otf_launch_count(void) { return g_launches.load(); }
 
 const char* otf_kernel_names(void) {
   return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;pq_scan16_xor;"
-         "pq_scan_generic;pq_scan16_f32bins;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
+         "pq_scan_generic;pq_scan16_f32bins;pq_encode_mma;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
          "bin_hamming;split_w_half_kernel;absmax_kernel;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
          "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local";
 }
@@ -896,6 +896,43 @@ int otf_binarize(int device, const double* frame, const float* centering, int32_
   return S.out(out, dout, (size_t)n * row_bytes, mem);
 }
 
+namespace {
+// per-thread, per-device scratch of the stateless calls, ordered by an event: no cudaMalloc /
+// cudaFree (an implicit device synchronisation, and occasionally tens of ms of host time) per call
+struct CachedScratchBuf {
+  DevBuf buf;
+  cudaEvent_t done = nullptr;
+  int device = 0;
+  ~CachedScratchBuf() {
+    if (done) {
+      cudaSetDevice(device);
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+    }
+    buf.release();
+  }
+  // a buffer of >= bytes usable on st once the previous call's work is done
+  int acquire(size_t bytes, cudaStream_t st, void** p) {
+    if (done && cudaStreamWaitEvent(st, done, 0) != cudaSuccess) return cuda_fail(cudaGetLastError(), "wait");
+    if (int rc = buf.ensure(bytes > 0 ? bytes : 16)) return rc;  // growing frees the old one (synchronises)
+    *p = buf.p;
+    return OTF_OK;
+  }
+  int release(cudaStream_t st) {
+    if (!done && cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "cudaEventCreate");
+    cudaEventRecord(done, st);
+    return OTF_OK;
+  }
+};
+CachedScratchBuf& cached_scratch(int device) {
+  static thread_local std::map<int, CachedScratchBuf> per_device;
+  CachedScratchBuf& c = per_device[device];
+  c.device = device;
+  return c;
+}
+}  // namespace
+
 int otf_pq_encode(int device, const float* vectors, int64_t n, int32_t dim, const float* centroids,
                   int32_t num_blocks, int32_t num_centroids, int32_t subdim, uint8_t* out_codes, int mem,
                   void* stream) {
@@ -913,10 +950,12 @@ int otf_pq_encode(int device, const float* vectors, int64_t n, int32_t dim, cons
   if ((rc = S.in(vectors, (size_t)n * dim * 4, mem, &dX))) return rc;
   if ((rc = S.in(centroids, cb, mem, &dc))) return rc;
   if ((rc = S.outbuf(out_codes, (size_t)n * num_blocks, mem, &dout))) return rc;
-  if ((rc = S.tmp(pq_encode_scratch_bytes(num_blocks, num_centroids), &dnorm))) return rc;
-  if ((rc = launch_pq_encode(static_cast<const float*>(dX), n, num_blocks, num_centroids, subdim,
-                             static_cast<const float*>(dc), dnorm, static_cast<uint8_t*>(dout), device, st)))
-    return rc;
+  CachedScratchBuf& cs = cached_scratch(device);
+  if ((rc = cs.acquire(pq_encode_scratch_bytes(num_blocks, num_centroids), st, &dnorm))) return rc;
+  rc = launch_pq_encode(static_cast<const float*>(dX), n, num_blocks, num_centroids, subdim,
+                        static_cast<const float*>(dc), dnorm, static_cast<uint8_t*>(dout), device, st);
+  if (int rc2 = cs.release(st)) return rc ? rc : rc2;
+  if (rc) return rc;
   return S.out(out_codes, dout, (size_t)n * num_blocks, mem);
 }
 

@@ -793,6 +793,173 @@ __global__ void __launch_bounds__(256) pq_encode_kernel(const float* __restrict_
   }
 }
 
+// ---- pq_encode with the dot products on the tensor cores (Q == 8, K <= 256) --------------------
+// The FFMA kernel above is energy-bound: 9 FFMA of dot product + 5 compare/select per (row,
+// centroid), and back-to-back launches run into power excursions (tools/enc_probe.py). Here the
+// x·c dots of a 16-row tile against 8 centroids are ONE legacy tensor-core tile (mma.sync
+// m16n8k8 TF32) with three split products (x_hi c_hi + x_hi c_lo + x_lo c_hi, v_hi = v with 13
+// low mantissa bits cleared: |dot error| <= 2^-18 sum|x_q c_q|), so only the distance and the
+// running (best, second-best) stay on the SIMT pipes. The centroid index rides in the low 8
+// mantissa bits of each distance (relative perturbation <= 2^-15), so the running minimum and
+// second minimum are 3 FMNMX per candidate with the argmin included. The float32 winner is
+// taken when the runner-up is more than 2 eps + the perturbation behind, eps = 2^-16 (max_j
+// |c_j|^2 + 2 |x| max_j |c_j|) (>2x the bound above); otherwise (near-ties, non-finite data) the
+// (row, block) is decided by encode_exact in float64 with numpy's semantics, as before.
+// One warp = 16 rows of one sub-quantizer; blockIdx.y = the sub-quantizer.
+constexpr int kEncMmaThreads = 256;
+
+// encode_exact for Q == 8 with the whole warp: lane l scores centroids l, l + 32, ... in float64
+// (the same arithmetic as encode_exact), then a warp argmin with numpy's semantics (the first
+// NaN if any, else the first minimum).
+__device__ int encode_exact_warp(const float* __restrict__ xs, const float* __restrict__ cg,
+                                 const double* __restrict__ ng, int K, int lane) {
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = (double)__ldg(xs + q);
+  int arg = -1;
+  double best = 0.0;
+  bool nan_seen = false;
+  for (int j = lane; j < K; j += 32) {
+    const float* c = cg + j * 8;
+    double dot = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dot = __fma_rn(x[q], (double)c[q], dot);
+    const double sq = __dsub_rn(ng[j], 2.0 * dot);
+    if (arg < 0) {
+      best = sq; arg = j; nan_seen = isnan(sq);
+    } else if (!nan_seen) {
+      if (isnan(sq)) { best = sq; arg = j; nan_seen = true; }
+      else if (sq < best) { best = sq; arg = j; }
+    }
+  }
+  // (nan first, then smaller value, then smaller index); lanes without a centroid lose
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    const bool on = __shfl_xor_sync(0xffffffffu, (int)nan_seen, o) != 0;
+    bool take;
+    if (oa < 0) take = false;
+    else if (arg < 0) take = true;
+    else if (nan_seen != on) take = on;
+    else if (nan_seen) take = oa < arg;
+    else take = ob < best || (ob == best && oa < arg);
+    if (take) { best = ob; arg = oa; nan_seen = on; }
+  }
+  return arg;
+}
+
+__device__ __forceinline__ void mma_tf32_m16n8k8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & 0xFFFFE000u; }
+__device__ __forceinline__ uint32_t tf32_lo(float v) { return __float_as_uint(__fsub_rn(v, __uint_as_float(tf32_hi(v)))); }
+// distance with the centroid index in its low 8 mantissa bits (padding: +inf -> a NaN pattern,
+// which fminf/fmaxf ignore)
+__device__ __forceinline__ float enc_key(float d, int j) {
+  return __uint_as_float((__float_as_uint(d) & ~0xFFu) | (uint32_t)j);
+}
+__device__ __forceinline__ void enc_upd(float& b, float& s, float k) {
+  s = fminf(s, fmaxf(b, k));
+  b = fminf(b, k);
+}
+
+__global__ void __launch_bounds__(kEncMmaThreads) pq_encode_mma(const float* __restrict__ X, int64_t n, int dim,
+                                                                const float* __restrict__ cents,
+                                                                const double* __restrict__ norms,
+                                                                const float* __restrict__ bounds, int M, int K,
+                                                                uint8_t* __restrict__ codes) {
+  constexpr int Q = 8;
+  const int m = blockIdx.y;
+  __shared__ __align__(16) uint4 sB[32 * 32];  // [n-tile][lane]: {hi(c[j][t4]), hi(c[j][t4+4]), lo(..), lo(..)}, j = 8nt+g
+  __shared__ __align__(16) float sC[256 * Q];  // natural layout (exact path)
+  __shared__ __align__(8) float sN[256];       // float32 norms, +inf past K
+  __shared__ double sN64[256];                 // float64 norms (exact path)
+  const float* cm = cents + (int64_t)m * K * Q;
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int l = e & 31, j = (e >> 5) * 8 + (l >> 2), t4 = l & 3;
+    const float c0 = j < K ? cm[j * Q + t4] : 0.f, c1 = j < K ? cm[j * Q + t4 + 4] : 0.f;
+    sB[e] = make_uint4(tf32_hi(c0), tf32_hi(c1), tf32_lo(c0), tf32_lo(c1));
+  }
+  for (int e = threadIdx.x; e < 256 * Q; e += blockDim.x) sC[e] = e < K * Q ? cm[e] : 0.f;
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) {
+    const double v = j < K ? norms[(int64_t)m * K + j] : 0.0;
+    sN64[j] = v;
+    sN[j] = j < K ? (float)v : __int_as_float(0x7f800000);
+  }
+  __syncthreads();
+  const float cmax2 = bounds[3 * m], cmax = bounds[3 * m + 1];
+  const bool bad = bounds[3 * m + 2] != 0.f;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int ntiles = (K + 7) >> 3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 16; r0 < n; r0 += warps * 16) {
+    const int64_t ra = r0 + g, rb = ra + 8;
+    const float* xa = X + (ra < n ? ra : n - 1) * dim + m * Q;
+    const float* xb = X + (rb < n ? rb : n - 1) * dim + m * Q;
+    const float xa0 = __ldg(xa + t4), xa1 = __ldg(xa + t4 + 4), xb0 = __ldg(xb + t4), xb1 = __ldg(xb + t4 + 4);
+    // A fragments (m16n8k8 row-major): a0 (row g, k t4), a1 (row g+8, k t4), a2 (row g, k t4+4), a3 (row g+8, k t4+4)
+    const uint32_t ah[4] = {tf32_hi(xa0), tf32_hi(xb0), tf32_hi(xa1), tf32_hi(xb1)};
+    const uint32_t al[4] = {tf32_lo(xa0), tf32_lo(xb0), tf32_lo(xa1), tf32_lo(xb1)};
+    float qa = fmaf(xa0, xa0, xa1 * xa1), qb = fmaf(xb0, xb0, xb1 * xb1);  // |x|^2 over the quad
+    qa += __shfl_xor_sync(0xffffffffu, qa, 1);
+    qb += __shfl_xor_sync(0xffffffffu, qb, 1);
+    qa += __shfl_xor_sync(0xffffffffu, qa, 2);
+    qb += __shfl_xor_sync(0xffffffffu, qb, 2);
+    const float inf = __int_as_float(0x7f800000);
+    float ba = inf, sa = inf, bb = inf, sb2 = inf;  // (best, second) keys of rows g and g+8
+    for (int nt = 0; nt < ntiles; ++nt) {
+      const uint4 f = sB[nt * 32 + lane];
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      mma_tf32_m16n8k8(acc, ah, f.x, f.y);
+      mma_tf32_m16n8k8(acc, ah, f.z, f.w);
+      mma_tf32_m16n8k8(acc, al, f.x, f.y);
+      const int j0 = nt * 8 + 2 * t4;  // C fragment: c0,c1 (row g, cols 2t4, 2t4+1), c2,c3 (row g+8)
+      const float2 nn = *reinterpret_cast<const float2*>(sN + j0);
+      enc_upd(ba, sa, enc_key(fmaf(-2.f, acc[0], nn.x), j0));
+      enc_upd(ba, sa, enc_key(fmaf(-2.f, acc[1], nn.y), j0 + 1));
+      enc_upd(bb, sb2, enc_key(fmaf(-2.f, acc[2], nn.x), j0));
+      enc_upd(bb, sb2, enc_key(fmaf(-2.f, acc[3], nn.y), j0 + 1));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {  // merge the quad's (best, second) pairs
+      const float oba = __shfl_xor_sync(0xffffffffu, ba, o), osa = __shfl_xor_sync(0xffffffffu, sa, o);
+      const float obb = __shfl_xor_sync(0xffffffffu, bb, o), osb = __shfl_xor_sync(0xffffffffu, sb2, o);
+      sa = fminf(fminf(sa, osa), fmaxf(ba, oba));
+      ba = fminf(ba, oba);
+      sb2 = fminf(fminf(sb2, osb), fmaxf(bb, obb));
+      bb = fminf(bb, obb);
+    }
+    // decide: lanes t4 == 0 hold rows g (h = 0) and g + 8 (h = 1)
+    bool amb[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = h ? rb : ra;
+      const float b = h ? bb : ba, s2 = h ? sb2 : sa;
+      const float eps = 0x1p-16f * (cmax2 + 2.f * sqrtf(h ? qb : qa) * cmax);
+      const float pert = 0x1p-14f * (fabsf(b) + fabsf(s2)) + 0x1p-140f;
+      const bool ok = !bad && s2 - b > 2.f * eps + pert;  // NaN fails this test
+      amb[h] = t4 == 0 && row < n && !ok;
+      if (t4 == 0 && row < n && ok) codes[row * M + m] = (uint8_t)(__float_as_uint(b) & 0xFFu);
+    }
+    // rare: near-ties / non-finite data — the whole warp computes that (row, block)'s float64
+    // distances (8 centroids per lane) and takes numpy's argmin
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      unsigned todo = __ballot_sync(0xffffffffu, amb[h]);
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t row = r0 + (src >> 2) + 8 * h;
+        const int code = encode_exact_warp(X + row * dim + (int64_t)m * Q, sC, sN64, K, lane);
+        if (lane == 0) codes[row * M + m] = (uint8_t)code;
+      }
+    }
+  }
+}
+
 // vectors (n, M*Q) float32, centroids (M, K, Q) float32 on the device -> codes (n, M) uint8.
 // scratch: M*K float64 norms + 3*M float32 bounds (pq_encode_scratch_bytes).
 size_t pq_encode_scratch_bytes(int M, int K) { return (size_t)M * K * 8 + (size_t)M * 3 * 4 + 16; }
@@ -808,6 +975,20 @@ int launch_pq_encode(const float* X, int64_t n, int M, int K, int Q, const float
   OTF_LAUNCH_CHECK("pq_cent_norms_kernel");
   pq_block_bounds_kernel<<<M, 256, 0, st>>>(cents, norms, M, K, Q, bounds);
   OTF_LAUNCH_CHECK("pq_block_bounds_kernel");
+  static const bool ffma = getenv("OTF_PQ_ENCODE_FFMA") != nullptr;  // A/B switch (tools/)
+  if (Q == 8 && !ffma) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pq_encode_mma, kEncMmaThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t bx = ((int64_t)per_sm * sm_count(device) + M - 1) / M;  // CTAs per sub-quantizer
+    const int64_t need = (n + (kEncMmaThreads / 32) * 16 - 1) / ((kEncMmaThreads / 32) * 16);
+    if (need < bx) bx = need;
+    if (bx < 1) bx = 1;
+    pq_encode_mma<<<dim3((unsigned)bx, (unsigned)M), kEncMmaThreads, 0, st>>>(X, n, M * Q, cents, norms, bounds, M,
+                                                                             K, codes);
+    OTF_LAUNCH_CHECK("pq_encode_mma");
+    return OTF_OK;
+  }
   const size_t Kp = (size_t)((K + 3) & ~3);
   const size_t per_m = Kp * Q * 4 + Kp * 12 + 16;
   const size_t budget = 200 * 1024;
