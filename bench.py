@@ -707,13 +707,15 @@ def run_encode(args, cfg):
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 screening, f64 decision", "data": "synthetic",
+            "vs_baseline": None, "dtype": "tf32x3 / f32 screening, f64 decision", "data": "synthetic",
             "config": {"workload": cfg["workload"], "rows_per_gpu": n, "dim": dim, "blocks": M,
                        "centroids": K, "subdim": Q, "l2": "inputs (%.1f GB/GPU) larger than L2" % (n * dim * 4 / 1e9)},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP32_PEAK_TFLOPS, "traffic": profile_traffic("c3e"),
                          "traffic_unit": "DRAM bytes per launch (ncu)",
-                         "kernel": "pq_encode_kernel<8>: 2*K*Q flop per vector and block (FFMA screening)",
+                         "kernel": ("pq_encode_mma: 2*K*Q useful flop per vector and block; the dots run as TF32x3 "
+                                    "mma.sync tiles, the per-centroid distance + running argmin (SIMT ALU) bound it; "
+                                    "peak = the FFMA form's bound"),
                          "hbm_gbs": n * (dim * 4 + M) / (ms / 1e3) / 1e9,
                          "peak_source": "derived: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (no measured FP32 peak)"},
             "cpu_baseline": cpu,
