@@ -471,7 +471,7 @@ def test_pq_encode_matches_reference_golden(otf, golden, name):
 
 
 @pytest.mark.parametrize("m,k,q,n", [(16, 256, 8, 20_000), (8, 256, 16, 5000), (3, 100, 7, 3000),
-                                     (2, 256, 40, 1000), (32, 256, 4, 4000)])
+                                     (2, 256, 40, 1000), (32, 256, 4, 4000), (4, 100, 8, 3001), (5, 3, 8, 777)])
 def test_pq_encode_matches_oracle(otf, m, k, q, n):
     rng = np.random.default_rng(m * 1000 + q)
     cents = rng.standard_normal((m, k, q)).astype(np.float32)
@@ -481,6 +481,18 @@ def test_pq_encode_matches_oracle(otf, m, k, q, n):
     gpu = otf.pq_encode(otf.PQCodebook(cents), vecs)
     assert _codes_agree(gpu, ref, gap, cents, vecs) <= max(1, n * m // 100_000)
     assert not np.any(gpu == 1)  # the duplicate of centroid 0 is never chosen
+
+
+@pytest.mark.parametrize("scale", [1e-20, 1e-3, 1e15])
+def test_pq_encode_magnitudes(otf, scale):
+    """Q = 8 runs on the tensor cores (TF32 split dots, index-in-mantissa argmin); extreme but
+    finite magnitudes must give the same codes as the float64 oracle."""
+    rng = np.random.default_rng(int(np.log10(scale)) + 40)
+    cents = (rng.standard_normal((4, 64, 8)) * scale).astype(np.float32)
+    vecs = (rng.standard_normal((2000, 32)) * scale).astype(np.float32)
+    ref, gap = O.pq_encode(cents, vecs)
+    gpu = otf.pq_encode(otf.PQCodebook(cents), vecs)
+    assert _codes_agree(gpu, ref, gap, cents, vecs) <= 1
 
 
 def test_pq_encode_errors_and_empty(otf):
