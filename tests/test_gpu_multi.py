@@ -133,7 +133,9 @@ def test_single_cta_path_matches_pair_path(otf, monkeypatch, form, n, d, c):
 
 
 @pytest.mark.parametrize("n,d,c,k", [(50_000, 64, 64, 1000), (3000, 32, 40, 3000), (9000, 96, 5, 8500),
-                                     (4000, 64, 70, 50), (600, 32, 130, 17)])
+                                     (4000, 64, 70, 50), (600, 32, 130, 17),
+                                     # larger segments (several gather passes per thread)
+                                     (70_001, 32, 16, 500), (140_000, 64, 64, 2000)])
 def test_rank_many_segmented_topk(otf, n, d, c, k):
     """rank_many selects all classifiers of a group in one segmented cooperative launch (two or
     more SMs per classifier); lists equal the oracle's top_k of the scores, including heavy ties
