@@ -69,7 +69,13 @@ constexpr int kASlots = 8;        // TMEM ring of 32-column x_lo slots
 // accumulation every 4 chunks (128 K values) and adding the group partials in float32 (RN) in the
 // epilogue brings it to numpy's own float32 sgemm level (0.055 vs 0.041 of the tolerance at
 // d = 4096; 0.155 vs 0.128 at d = 512) at ~1-3% of kernel time (tools/multi_err.py).
-constexpr int kGroupChunks = 4;
+// FP16 form, measured against the exact dot (tools/multi_err.py, max over 20k rows x 64
+// classifiers, fraction of the tolerance): 4 chunks 0.029 / 0.064 (d = 4096 / 512), 8 chunks
+// 0.032 / 0.111, 16 chunks 0.055 / 0.186; numpy's own float32 sgemm: 0.041 / 0.128. 8 keeps
+// the error below numpy's and halves the epilogue's group adds (C5b -2.5% under the power cap).
+// The TF32 form keeps 4.
+template <bool H>
+constexpr int group_chunks() { return H ? 8 : 4; }
 constexpr int kTileX = kMT * kKC * 4;  // 16 KB
 constexpr int kMultiThreads = 512;
 constexpr int kTmemCols = 512;
@@ -434,16 +440,16 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
     if (rank == 0) {
       const uint64_t wdesc0 = H ? umma_desc_sw64(smem_u32(wring)) : umma_desc_sw128(smem_u32(wring));
       const uint64_t xdesc0 = umma_desc_sw128(smem_u32(xring));
-      // accumulation restarts every kGroupChunks chunks in the other accumulator; the epilogue
+      // accumulation restarts every group_chunks<H>() chunks in the other accumulator; the epilogue
       // adds the group partials in float32 (round to nearest)
       uint32_t it = 0, j = 0;
       for (int64_t t = unit; t < n_tiles; t += n_units) {
-        for (int g0 = 0; g0 < kchunks; g0 += kGroupChunks, ++j) {
+        for (int g0 = 0; g0 < kchunks; g0 += group_chunks<H>(), ++j) {
           const int b = j & 1;
           mbar_wait(&tmem_empty[b], ((j >> 1) & 1u) ^ 1u);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t acc = tmem_base + b * 128;
-          const int g1 = g0 + kGroupChunks < kchunks ? g0 + kGroupChunks : kchunks;
+          const int g1 = g0 + group_chunks<H>() < kchunks ? g0 + group_chunks<H>() : kchunks;
           for (int kc = g0; kc < g1; ++kc, ++it) {
             const int s = it % C::kWStages, sx = it % kXStages, a = it % kASlots;
             mbar_wait(&wfull[s], (it / C::kWStages) & 1u);  // W (both halves) landed
@@ -472,7 +478,7 @@ multi_score_tc(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
       float sum[64];
 #pragma unroll
       for (int c = 0; c < 64; ++c) sum[c] = 0.f;
-      for (int g0 = 0; g0 < kchunks; g0 += kGroupChunks, ++j) {
+      for (int g0 = 0; g0 < kchunks; g0 += group_chunks<H>(), ++j) {
         const int b = j & 1;
         mbar_wait(&tmem_full[b], (j >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;");
