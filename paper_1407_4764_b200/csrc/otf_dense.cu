@@ -166,7 +166,7 @@ int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, fl
       case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st, cmax, clog);
       case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st, cmax, clog);
       case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st, cmax, clog);
-      case 16: return launch_fast<16, 1>(X, n, w, out, hist, device, st, cmax, clog);
+      case 16: return launch_fast<16, 2>(X, n, w, out, hist, device, st, cmax, clog);  // R 1 / 4: +0.6% / +2.8%
       case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st, cmax, clog);
       default: break;
     }
