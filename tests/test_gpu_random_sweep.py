@@ -66,3 +66,50 @@ def test_random_rank(otf, seed):
     o_ids, o_sc, _ = O.top_k(s, k, ids)
     np.testing.assert_array_equal(r.ids, o_ids)
     np.testing.assert_array_equal(r.scores, np.asarray(o_sc, np.float64))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_rank_many(otf, seed):
+    """score_many / rank_many: random sizes (partial 128-row tiles, odd n), dims (multiples of
+    32), classifier counts (1..130: several 64-classifier groups), k (0, > n)."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([129, 1000, 4097, 20_001]))
+    d = int(rng.choice([32, 96, 512]))
+    c = int(rng.choice([1, 7, 64, 65, 130]))
+    k = int(rng.choice([0, 1, 100, n + 1]))
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    W = rng.standard_normal((c, d))
+    ids = rng.permutation(2 * n)[:n].astype(np.int64) if seed % 2 else None
+    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    S = repo.score_many(list(W))
+    ex = (x.astype(np.float64) @ W.astype(np.float32).astype(np.float64).T).T
+    mag = np.abs(W.astype(np.float32).astype(np.float64)) @ np.abs(x.astype(np.float64)).T
+    assert np.all(np.abs(S - ex) <= 2.0 ** -20 * mag + np.spacing(np.abs(S)) + 1e-30)
+    lists = repo.rank_many([otf.LinearModel(w, 1, 1) for w in W], k)
+    for i in range(c):
+        o_ids, o_sc, _ = O.top_k(S[i], k, ids)
+        np.testing.assert_array_equal(lists[i].ids, o_ids)
+        np.testing.assert_array_equal(lists[i].scores, np.asarray(o_sc, np.float64))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_pq_encode(otf, seed):
+    """pq_encode: random block counts, centroid counts (<= 256, not multiples of 8), sub-dims (the
+    tensor-core form for Q = 8, the FFMA form otherwise) and scales; codes equal the float64
+    oracle's except at rounding-level near-ties."""
+    rng = np.random.default_rng(2000 + seed)
+    m = int(rng.choice([1, 3, 16]))
+    k = int(rng.choice([1, 5, 100, 256]))
+    q = int(rng.choice([4, 8, 8, 16]))
+    n = int(rng.choice([1, 31, 1000, 5003]))
+    scale = float(10.0 ** rng.integers(-3, 4))
+    cents = (rng.standard_normal((m, k, q)) * scale).astype(np.float32)
+    vecs = (rng.standard_normal((n, m * q)) * scale).astype(np.float32)
+    ref, _ = O.pq_encode(cents, vecs)
+    gpu = otf.pq_encode(otf.PQCodebook(cents), vecs)
+    for i, b in np.argwhere(gpu != ref):  # a differing code must be a rounding-level near-tie
+        x = vecs[i, b * q:(b + 1) * q].astype(np.float64)
+        c = cents[b].astype(np.float64)
+        dist = (c * c).sum(1) - 2.0 * (c @ x)
+        a, r = dist[int(gpu[i, b])], dist[int(ref[i, b])]
+        assert abs(a - r) <= 1e-12 * max(1.0, abs(a), abs(r)), (i, b, a, r)
