@@ -49,6 +49,8 @@ __device__ __forceinline__ double lut_entry_einsum(const float* __restrict__ c,
 // lut is (M, K) row-major float64 (the reference's layout).
 __global__ void pq_build_lut_kernel(const float* __restrict__ cents, int M, int K, int Q,
                                     const double* __restrict__ w, double* __restrict__ lut) {
+  // the dependent scan (programmatic launch) may start its own setup now
+  asm volatile("griddepcontrol.launch_dependents;");
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= M * K) return;
   const int m = t / K;
@@ -409,6 +411,9 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
   if (threadIdx.x < 16) smax[threadIdx.x] = 0u;
   hist_zero(sh);
   __syncthreads();
+  // launched programmatically after the LUT kernel: wait for its writes before reading lut_g
+  // (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     // thread t always handles sub-quantizer m = t & 15 (blockDim = 512): 16 lanes fill one
     // 128-byte run of a line, and the per-m maxima need one atomic per thread
@@ -593,7 +598,18 @@ int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int 
   int64_t grid = (int64_t)per_sm[device & 63] * sm_count(device);
   const int64_t need = (n + kScanF32Threads * ROWS - 1) / (kScanF32Threads * ROWS);
   if (need < grid) grid = need;
-  fn<<<(int)grid, kScanF32Threads, kScanF32Smem, st>>>(codes, n, lut, K, bins, hist, cmax);
+  static const bool no_pdl = getenv("OTF_PQ_NO_PDL") != nullptr;  // A/B switch (tools/)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kScanF32Threads);
+  cfg.dynamicSmemBytes = kScanF32Smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the LUT kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, codes, n, lut, K, bins, hist, cmax));
   if (cmax && clog) *clog = 7;  // 32 * ROWS rows per chunk
   OTF_LAUNCH_CHECK("pq_scan16_f32bins");
   return OTF_OK;
