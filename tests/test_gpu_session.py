@@ -69,3 +69,21 @@ def test_device_snapshot_publication_equals_host_snapshot(otf, golden):
     small = otf.Repository.dense(otf.FeatureStore(np.ones((10, 16), np.float32)))
     with _pytest.raises(otf.ConfigError):
         tr.publish_to(small)
+
+
+def test_published_and_host_ranks_interleave_across_k(otf, golden):
+    """rank_published (trainer-published device w) and host-memory rank share the repository's
+    graph cache: interleaving them with k growing past the 8192-candidate layout and back must
+    keep every list equal to the oracle-equivalent host rank of the same snapshot."""
+    x = np.random.default_rng(11).standard_normal((20_000, golden["sess_test_x"].shape[1])).astype(np.float32)
+    repo = otf.Repository.dense(otf.FeatureStore(x))
+    tr = otf.OnlineTrainer(repo.model_dim, golden["sess_neg"], otf.TrainerConfig(lam=0.1, batch_size=16, seed=5))
+    tr.append_positives(golden["sess_feed"][:5])
+    n = repo.count
+    for step, k in enumerate([10, 25, min(n, 9000), 10, min(n, 12_000), 3]):
+        tr.step()
+        _, ver = tr.publish_to(repo)
+        snap = tr.snapshot()
+        a = repo.rank_published(k, model_version=ver)
+        b = repo.rank(snap, k)
+        assert list(a.ids) == list(b.ids) and np.array_equal(a.scores, b.scores), (step, k)
