@@ -515,7 +515,7 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   else
     rc = score_into(r, w_dev, r->scores.p, r->topk.hist, st, r->topk.cmax, &clog);
   cudaEventRecord(e1, st);
-  if (!rc) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBins * sizeof(uint32_t), st) == cudaSuccess
+  if (!rc) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBinsMax * sizeof(uint32_t), st) == cudaSuccess
                     ? OTF_OK : cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
   cudaError_t e = cudaEventSynchronize(e1);
   if (!rc && e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);

@@ -58,8 +58,18 @@ constexpr int kHistBins = 4096;
 __device__ __forceinline__ uint32_t hist_bin(float s) { return (uint32_t)(score_key(s) >> 20); }
 __device__ __forceinline__ uint32_t hist_bin(double s) { return hist_bin(__double2float_rn(s)); }
 
-__device__ __forceinline__ void hist_zero(uint32_t* sh) {
-  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0u;
+// The PQ rank path (exact bins, otf_pq.cu pq_scan16_f32bins) uses 13 key bits / 8192 bins: its
+// threshold bin holds about half the rows, so the top-k ranks about half the candidates; the
+// dense and binary scans keep 4096 bins (their scans pay for a larger histogram more than their
+// top-k gains). kHistBinsMax sizes the shared workspace.
+constexpr int kPqHistBits = 13;
+constexpr int kPqHistBins = 1 << kPqHistBits;
+constexpr int kHistBinsMax = kPqHistBins;
+__device__ __forceinline__ uint32_t pq_hist_bin(float s) { return (uint32_t)(score_key(s) >> (32 - kPqHistBits)); }
+__device__ __forceinline__ uint32_t pq_hist_bin(double s) { return pq_hist_bin(__double2float_rn(s)); }
+
+__device__ __forceinline__ void hist_zero(uint32_t* sh, int nb = kHistBins) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0u;
 }
 // Shared-memory histogram update. Plain per-lane ATOMS: the scores of neighbouring rows
 // rarely share a bin, and __match_any_sync (ADU pipe) cost more than the replays it saves
@@ -67,8 +77,8 @@ __device__ __forceinline__ void hist_zero(uint32_t* sh) {
 __device__ __forceinline__ void hist_add(uint32_t* sh, bool active, uint32_t bin) {
   if (active) atomicAdd(&sh[bin], 1u);
 }
-__device__ __forceinline__ void hist_flush(const uint32_t* sh, uint32_t* g) {
-  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
+__device__ __forceinline__ void hist_flush(const uint32_t* sh, uint32_t* g, int nb = kHistBins) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
     if (sh[b]) atomicAdd(&g[b], sh[b]);
 }
 

@@ -397,7 +397,7 @@ static int launch_scan16(const uint8_t* codes, int64_t n, const float* cents, co
 // (l >> 4): 32 lanes hit 32 different banks (one wavefront per LDS.32), and the whole
 // address is ONE byte_perm (code byte -> bits 8..15, a per-lane constant in bits 0..7).
 constexpr int kScanF32Threads = 512;
-constexpr size_t kScanF32Smem = 256 * 256 + kHistBins * sizeof(uint32_t) + 32 * sizeof(uint32_t);
+constexpr size_t kScanF32Smem = 256 * 256 + kPqHistBins * sizeof(uint32_t) + 32 * sizeof(uint32_t);
 
 template <int ROWS>
 __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const uint8_t* __restrict__ codes, int64_t n,
@@ -407,9 +407,9 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
                                                                      uint16_t* __restrict__ cmax) {
   extern __shared__ __align__(256) unsigned char sm[];  // [256 lines x 256 B][hist][m maxima]
   uint32_t* sh = reinterpret_cast<uint32_t*>(sm + 65536);
-  uint32_t* smax = sh + kHistBins;
+  uint32_t* smax = sh + kPqHistBins;
   if (threadIdx.x < 16) smax[threadIdx.x] = 0u;
-  hist_zero(sh);
+  hist_zero(sh, kPqHistBins);
   __syncthreads();
   // launched programmatically after the LUT kernel: wait for its writes before reading lut_g
   // (a no-op for a normal launch)
@@ -515,13 +515,13 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
       // [lo, hi] inside one bin <=> their order keys agree in the top 12 bits <=> their bit
       // patterns do (same sign; -0.0 vs +0.0 counts as different: conservative)
       const float lo = __fsub_rd(s32[i], eps), hi = __fadd_ru(s32[i], eps);
-      if (!screen || (__float_as_uint(lo) ^ __float_as_uint(hi)) >= (1u << 20)) need_exact |= 1u << i;
+      if (!screen || (__float_as_uint(lo) ^ __float_as_uint(hi)) >= (1u << (32 - kPqHistBits))) need_exact |= 1u << i;
     }
     uint32_t bin[ROWS];
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {  // order key of a float without the -0.0 test (done above)
       const uint32_t v = __float_as_uint(s32[i]);
-      bin[i] = (v ^ ((uint32_t)((int32_t)v >> 31) | 0x80000000u)) >> 20;
+      bin[i] = (v ^ ((uint32_t)((int32_t)v >> 31) | 0x80000000u)) >> (32 - kPqHistBits);
     }
     // 2) rare: rows whose interval straddles a bin edge take the exact float64 score (numpy's
     //    pairwise order) and its bin
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
           double rr[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
-          bin[i] = hist_bin(__dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+          bin[i] = pq_hist_bin(__dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
                                       __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7]))));
         }
       }
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
   }
   if (ghist) {
     __syncthreads();
-    hist_flush(sh, ghist);
+    hist_flush(sh, ghist, kPqHistBins);
   }
 }
 
@@ -582,8 +582,6 @@ bool pq_bins_path(int M, const uint8_t* codes) { return M == 16 && pq_fast_path(
 int launch_pq_scan_bins(const uint8_t* codes, int64_t n, const double* lut, int K, uint16_t* bins,
                         uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax, int* clog) {
   if (n <= 0) return OTF_OK;
-  static const bool f64_bins = getenv("OTF_PQ_F64_BINS") != nullptr;  // A/B switch (tools/)
-  if (f64_bins) return launch_scan16(codes, n, nullptr, nullptr, lut, K, 0, nullptr, bins, hist, device, st);
   // 4 rows per thread (software-pipelined, ~112 registers, one 512-thread CTA per SM); 2 rows at
   // 64 registers (two CTAs per SM) rematerialises the per-lane constants and ran 33% slower
   constexpr int ROWS = 4;

@@ -5,7 +5,8 @@
 // full sort. Output scores are float64 (ranker.py:141), ids int64.
 //
 // One cooperative launch (persistent grid, one 1024-thread CTA per SM):
-//   A. coarse 4096-bin histogram of the scores (top 12 bits of the float32 order key) — this
+//   A. coarse 4096-bin histogram of the scores (top 12 bits of the float32 order key; PQ bins:
+//      8192 / 13 bits, written by the scan) — this
 //      phase is skipped when the scoring kernel already produced it (the fused path);
 //   B. every CTA scans the histogram from the top and finds the bin b0 holding the k-th
 //      entry, the count above it and its size: C = above + |b0| candidates;
@@ -98,6 +99,7 @@ template <typename ST>
 struct DirectSrc {
   using T = ST;
   static constexpr int kLoadBytes = sizeof(ST);
+  static constexpr int kBins = kHistBins;
   const ST* s;
   __device__ __forceinline__ void shift(int64_t o) { s += o; }
   __device__ __forceinline__ ST load(int64_t i) const { return __ldcg(s + i); }
@@ -132,6 +134,7 @@ struct DirectSrc {
 struct PqBinSrc {
   using T = double;
   static constexpr int kLoadBytes = 2;
+  static constexpr int kBins = kPqHistBins;  // bins written by pq_scan16_f32bins
   const uint16_t* bins; const uint8_t* codes; const double* lut; int M, K;
   __device__ __forceinline__ void shift(int64_t) {}  // one segment only
   __device__ __forceinline__ uint32_t load(int64_t i) const { return __ldcg(bins + i); }
@@ -161,10 +164,10 @@ struct PqBinSrc {
 
 // Workspace of segment `seg`: per segment one block of kWsWords counters (histogram, radix
 // histograms, barrier, count) and `cap` candidate slots.
-constexpr int64_t kWsWords = kHistBins + 3 * 256 + 4;
+constexpr int64_t kWsWords = kHistBinsMax + 3 * 256 + 4;
 __device__ __forceinline__ TopkWs seg_ws(TopkWs ws, unsigned seg) {
   ws.hist += (int64_t)seg * kWsWords;
-  ws.rhist = ws.hist + kHistBins;
+  ws.rhist = ws.hist + kHistBinsMax;
   ws.bar = reinterpret_cast<unsigned int*>(ws.rhist + 3 * 256);
   ws.count = ws.bar + 2;
   ws.key += (int64_t)seg * ws.cap;
@@ -191,15 +194,16 @@ __device__ __forceinline__ void append_candidate(const TopkWs& ws, bool take, ui
   }
 }
 
-// Block-wide: bins scanned from 4095 down; finds the bin where the running count reaches
-// `need`. Thread t owns bins 4095-BPT*t .. 4096-BPT*(t+1).
-constexpr int kBPT = kHistBins / kTopkThreads;
-__device__ void find_bin4096(const uint32_t* h, int64_t need, int* out_b, int64_t* out_above,
-                             int64_t* out_cnt, int64_t* wsum) {
+// Block-wide: bins scanned from NB-1 down; finds the bin where the running count reaches
+// `need`. Thread t owns bins NB-1-BPT*t .. NB-BPT*(t+1).
+template <int NB>
+__device__ void find_bin(const uint32_t* h, int64_t need, int* out_b, int64_t* out_above,
+                         int64_t* out_cnt, int64_t* wsum) {
+  constexpr int kBPT = NB / kTopkThreads;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   int64_t local = 0;
 #pragma unroll
-  for (int q = 0; q < kBPT; ++q) local += h[4095 - kBPT * t - q];
+  for (int q = 0; q < kBPT; ++q) local += h[NB - 1 - kBPT * t - q];
   int64_t incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -224,7 +228,7 @@ __device__ void find_bin4096(const uint32_t* h, int64_t need, int* out_b, int64_
   if (excl < need && incl >= need) {
     int64_t cum = excl;
     for (int q = 0; q < kBPT; ++q) {
-      const int bin = 4095 - kBPT * t - q;
+      const int bin = NB - 1 - kBPT * t - q;
       if (cum + h[bin] >= need) {
         *out_b = bin;
         *out_above = cum;
@@ -384,7 +388,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
   grid_barrier(ws.bar, nb);
   if (vb == 0) {
     for (int t = threadIdx.x; t < 3 * 256; t += blockDim.x) ws.rhist[t] = 0u;
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
+    for (int b = threadIdx.x; b < kHistBinsMax; b += blockDim.x) ws.hist[b] = 0u;
   }
   if (k_eff <= kCandCap) {
     if (vb == 0 && threadIdx.x == 0) *ws.count = 0u;
@@ -499,9 +503,9 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
   uint32_t b0 = 0;
   if (!all) {
     uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = __ldcg(ws.hist + b);
+    for (int b = threadIdx.x; b < Src::kBins; b += blockDim.x) sh[b] = __ldcg(ws.hist + b);
     __syncthreads();
-    find_bin4096(sh, k_eff, &s_b, &s_above, &s_cnt, wsum);
+    find_bin<Src::kBins>(sh, k_eff, &s_b, &s_above, &s_cnt, wsum);
     __syncthreads();
     b0 = (uint32_t)s_b;
     C = s_above + s_cnt;
@@ -611,7 +615,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
     grid_barrier(ws.bar, nb);
     TOPK_STAMP(3);
     if (vb == 0) {  // every CTA has read hist and count is no longer needed
-      for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
+      for (int b = threadIdx.x; b < kHistBinsMax; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
     rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
@@ -665,7 +669,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
     grid_barrier(ws.bar, nb);
     TOPK_STAMP(3);
     if (vb == 0) {  // every CTA has read hist and count is no longer needed
-      for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) ws.hist[b] = 0u;
+      for (int b = threadIdx.x; b < kHistBinsMax; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
     rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
@@ -695,7 +699,7 @@ int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg) {
     const size_t bytes = (size_t)n_seg * kWsWords * sizeof(uint32_t);
     OTF_CUDA(cudaMalloc(&ws->hist, bytes));
     OTF_CUDA(cudaMemset(ws->hist, 0, bytes));
-    ws->rhist = ws->hist + kHistBins;
+    ws->rhist = ws->hist + kHistBinsMax;
     ws->bar = reinterpret_cast<unsigned int*>(ws->rhist + 3 * 256);
     ws->count = ws->bar + 2;
     ws->n_seg = n_seg;
