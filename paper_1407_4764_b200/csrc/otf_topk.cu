@@ -195,47 +195,57 @@ __device__ __forceinline__ void append_candidate(const TopkWs& ws, bool take, ui
 }
 
 // Block-wide: bins scanned from NB-1 down; finds the bin where the running count reaches
-// `need`. Thread t owns bins NB-1-BPT*t .. NB-BPT*(t+1).
+// `need`. Thread t owns the kBPT contiguous bins NB-kBPT*(t+1) .. NB-1-kBPT*t, read straight from
+// the global histogram into registers (16-byte loads; one L2 round trip, no shared staging).
 template <int NB>
-__device__ void find_bin(const uint32_t* h, int64_t need, int* out_b, int64_t* out_above,
+__device__ void find_bin(const uint32_t* gh, int64_t need, int* out_b, int64_t* out_above,
                          int64_t* out_cnt, int64_t* wsum) {
   constexpr int kBPT = NB / kTopkThreads;
+  static_assert(kBPT % 4 == 0, "16-byte histogram loads");
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int base = NB - kBPT * (t + 1);
+  uint32_t v[kBPT];
+#pragma unroll
+  for (int u = 0; u < kBPT / 4; ++u) {
+    const uint4 q = __ldcg(reinterpret_cast<const uint4*>(gh + base) + u);
+    v[4 * u] = q.x; v[4 * u + 1] = q.y; v[4 * u + 2] = q.z; v[4 * u + 3] = q.w;
+  }
   int64_t local = 0;
 #pragma unroll
-  for (int q = 0; q < kBPT; ++q) local += h[NB - 1 - kBPT * t - q];
+  for (int q = 0; q < kBPT; ++q) local += v[q];
   int64_t incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+    const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
   }
   if (lane == 31) wsum[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    const int64_t v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-    int64_t s = v;
+    const int64_t u = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+    int64_t s = u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += u;
+      const int64_t w = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += w;
     }
-    wsum[lane] = s - v;  // exclusive prefix of warp sums
+    wsum[lane] = s - u;  // exclusive prefix of warp sums
   }
   __syncthreads();
   incl += wsum[wid];
   const int64_t excl = incl - local;
   if (excl < need && incl >= need) {
     int64_t cum = excl;
-    for (int q = 0; q < kBPT; ++q) {
-      const int bin = NB - 1 - kBPT * t - q;
-      if (cum + h[bin] >= need) {
-        *out_b = bin;
+#pragma unroll
+    for (int q = kBPT - 1; q >= 0; --q) {
+      if (cum >= 0 && cum + v[q] >= need) {
+        *out_b = base + q;
         *out_above = cum;
-        *out_cnt = h[bin];
-        break;
+        *out_cnt = v[q];
+        cum = -1;  // found (keeps the loop unrolled: v stays in registers)
+      } else if (cum >= 0) {
+        cum += v[q];
       }
-      cum += h[bin];
     }
   }
 }
@@ -502,10 +512,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
   int64_t C = n;
   uint32_t b0 = 0;
   if (!all) {
-    uint32_t* sh = reinterpret_cast<uint32_t*>(dyn);
-    for (int b = threadIdx.x; b < Src::kBins; b += blockDim.x) sh[b] = __ldcg(ws.hist + b);
-    __syncthreads();
-    find_bin<Src::kBins>(sh, k_eff, &s_b, &s_above, &s_cnt, wsum);
+    find_bin<Src::kBins>(ws.hist, k_eff, &s_b, &s_above, &s_cnt, wsum);
     __syncthreads();
     b0 = (uint32_t)s_b;
     C = s_above + s_cnt;
