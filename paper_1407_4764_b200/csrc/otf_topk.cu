@@ -304,12 +304,14 @@ __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k
   for (int64_t q = wid; q < mine; q += nw) {
     const int64_t i = vb + q * vnb;
     const uint64_t ki = sk[i], ii = si[i];
-    int64_t cnt = 0;
-    for (int64_t j = lane; j < m; j += 32) cnt += cand_greater(sk[j], si[j], ki, ii);
+    const int64_t r = lane == 0 ? __ldcg(ws.row + i) : 0;  // in flight during the count
+    int cnt = 0;
+    const int mm = (int)m;  // m <= kCandCap
+#pragma unroll 4
+    for (int j = lane; j < mm; j += 32) cnt += cand_greater(sk[j], si[j], ki, ii);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0 && cnt < k_eff) {
-      const int64_t r = __ldcg(ws.row + i);
       out_ids[cnt] = (int64_t)~ii;
       out_scores[cnt] = src.out_score(r, ki);
       if (out_rows) out_rows[cnt] = r;
