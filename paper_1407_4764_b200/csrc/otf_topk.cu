@@ -293,22 +293,23 @@ __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k
                           int64_t* out_rows, unsigned vb, unsigned vnb) {
   const int64_t mine = m > vb ? (m - 1 - vb) / vnb + 1 : 0;
   if (mine == 0) return;
-  uint64_t* sk = reinterpret_cast<uint64_t*>(dyn);
-  uint64_t* si = sk + m;
-  for (int64_t t = threadIdx.x; t < m; t += blockDim.x) {
-    sk[t] = __ldcg(ws.key + t);
-    si[t] = __ldcg(ws.inv + t);
-  }
+  ulonglong2* sc = reinterpret_cast<ulonglong2*>(dyn);  // (key, inv) pairs: one 16-byte load each
+  for (int64_t t = threadIdx.x; t < m; t += blockDim.x)
+    sc[t] = make_ulonglong2(__ldcg(ws.key + t), __ldcg(ws.inv + t));
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t q = wid; q < mine; q += nw) {
     const int64_t i = vb + q * vnb;
-    const uint64_t ki = sk[i], ii = si[i];
+    const ulonglong2 ci = sc[i];
+    const uint64_t ki = ci.x, ii = ci.y;
     const int64_t r = lane == 0 ? __ldcg(ws.row + i) : 0;  // in flight during the count
     int cnt = 0;
     const int mm = (int)m;  // m <= kCandCap
 #pragma unroll 4
-    for (int j = lane; j < mm; j += 32) cnt += cand_greater(sk[j], si[j], ki, ii);
+    for (int j = lane; j < mm; j += 32) {
+      const ulonglong2 cj = sc[j];
+      cnt += cand_greater(cj.x, cj.y, ki, ii);
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0 && cnt < k_eff) {
