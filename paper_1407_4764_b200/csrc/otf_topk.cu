@@ -129,6 +129,7 @@ struct DirectSrc {
   __device__ __forceinline__ double out_score(int64_t row, uint64_t) const {
     return (double)__ldcg(s + row);  // keeps a caller's -0.0 bit pattern
   }
+  __device__ __forceinline__ void prefetch_chunk(int64_t, int, int64_t, int) const {}
 };
 
 struct PqBinSrc {
@@ -160,6 +161,12 @@ struct PqBinSrc {
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
   }
   __device__ __forceinline__ double out_score(int64_t, uint64_t key) const { return key_to_f64(key); }
+  // the codes of a hit chunk (16 B per row) are pulled into L2 while its bins are read, so
+  // exact() of its candidates does not wait on a second HBM round trip
+  __device__ __forceinline__ void prefetch_chunk(int64_t r0, int CH, int64_t n, int lane) const {
+    if (8 * lane < CH && r0 + 8 * lane < n)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(codes + (r0 + 8 * lane) * 16));
+  }
 };
 
 // Workspace of segment `seg`: per segment one block of kWsWords counters (histogram, radix
@@ -579,6 +586,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
 #pragma unroll
         for (int j = 0; j < KB; ++j) {
           r0[j] = h + j < H ? (cb + list[h + j]) << ws.clog : n;  // n: empty slot
+          src.prefetch_chunk(r0[j], CH, n, lane);
 #pragma unroll
           for (int q = 0; q < RPL; ++q) {
             const int64_t i = r0[j] + 32 * q + lane;

@@ -4,7 +4,7 @@ F=paper_1407_4764_b200/csrc/otf_topk.cu
 cp $F /tmp/new_topk.cu
 run() {
   python -c "from paper_1407_4764_b200 import _build; _build.build(force=True)" > /dev/null 2>&1
-  for c in c3 c1 c5a; do
+  for c in c3 c1; do
     for rep in 1 2; do
       echo "$1 $c $(timeout 600 python bench.py --config $c --steps 200 --warmup 20 --no-cpu 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d["ms_per_step"]*1e3)')"
     done
