@@ -16,6 +16,9 @@
  *     memory; the call is synchronous and copies in/out) or OTF_MEM_DEVICE (device pointers on
  *     the handle's device; the call is asynchronous on `stream`, a cudaStream_t passed as
  *     void*; NULL is the legacy default stream, as everywhere in CUDA).
+ *   - A repository handle serialises its calls (one lock per handle) and orders them on the
+ *     GPU: a call on a different stream than the handle's previous call waits (CUDA event) for
+ *     that call's work, so the handle's shared workspaces are never used by two streams at once.
  *   - Scores are computed with the semantics of the reference: dense/binary scores are
  *     float32 of <x, float32(w)> (ranker.py:69, :89-93), PQ scores are float64 of the
  *     float64 LUT sum (pq.py:248-276). Ranked lists order by (-score, id) with ties toward
@@ -227,13 +230,16 @@ int otf_trainer_weights_ptr(otf_trainer* tr, const double** out);
 /* The trainer's CUDA stream (high priority; runs concurrently with ranking). */
 int otf_trainer_stream(otf_trainer* tr, void** out);
 /* Snapshot publication without a host round trip (SURVEY.md §8b threading; the device side of
- * trainer.py:161-173): copy the trainer's current w into the repository's snapshot buffer on the
- * trainer stream (ordered after every step already enqueued) and make the repository's stream
- * wait for it (CUDA event). The trainer keeps stepping on its own buffer meanwhile. */
+ * trainer.py:161-173): copy the trainer's current w into the TRAINER's snapshot buffer on the
+ * trainer stream (ordered after every step already enqueued) and record an event. `repo` is only
+ * checked for device and dim. The trainer keeps stepping on its own buffer meanwhile. */
 int otf_trainer_publish(otf_trainer* tr, otf_repo* repo);
-/* rank(k) under the last published snapshot (ranker.py:272-281), host outputs. */
-int otf_repo_rank_published(otf_repo* repo, int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
-                            int64_t* out_n);
+/* rank(k) under `tr`'s last published snapshot (ranker.py:272-281, session.py:197-218), host
+ * outputs: the repository's stream waits for the publication, copies it into the repository's
+ * ranking buffer and ranks, all under the repository's lock — sessions sharing one repository
+ * (service.py:91) never rank under each other's weights. NOT_READY before the first publish. */
+int otf_repo_rank_published(otf_repo* repo, otf_trainer* tr, int64_t k, int64_t* out_ids, double* out_scores,
+                            int64_t* out_rows, int64_t* out_n);
 
 /* ---- PQ codebook learning (learn_pq_codebook / _lloyd, pq.py:116-203) --------------------------
  * A handle keeps one block's float64 training sub-vectors (n, dim) on the device. Each step is

@@ -87,7 +87,7 @@ SIGNATURES: dict[str, list] = {
     "otf_trainer_weights_ptr": [_vp, _P(_vp)],
     "otf_trainer_stream": [_vp, _P(_vp)],
     "otf_trainer_publish": [_vp, _vp],
-    "otf_repo_rank_published": [_vp, _i64, _vp, _vp, _vp, _P(_i64)],
+    "otf_repo_rank_published": [_vp, _vp, _i64, _vp, _vp, _vp, _P(_i64)],
     "otf_pq_encode": [_int, _vp, _i64, _i32, _vp, _i32, _i32, _i32, _vp, _int, _vp],
     "otf_kmeans_create": [_int, _vp, _i64, _i32, _i32, _P(_vp)],
     "otf_kmeans_load": [_vp, _vp],

@@ -135,6 +135,12 @@ struct otf_repo {
   };
   std::vector<GraphEntry> graphs;  // <= kGraphCache entries, least recently used replaced
   uint64_t graph_clock = 0;
+  // Cross-stream ordering of the handle's workspaces (scores, bins, lut, histogram, barrier word,
+  // candidate slots): every call records `last` on the stream it used, and a call on a different
+  // stream waits for it first, so two calls on two streams never share a workspace on the GPU.
+  cudaEvent_t last = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool used = false;
 };
 
 struct otf_trainer {
@@ -147,7 +153,9 @@ struct otf_trainer {
   int neg_dtype = OTF_F32;
   int64_t n_neg = 0;
   int64_t n_pos = 0, pos_cap = 0;
+  DevBuf wsnap;                     // the published snapshot of w (otf_trainer_publish)
   cudaEvent_t published = nullptr;  // recorded after each snapshot copy (otf_trainer_publish)
+  cudaEvent_t consumed = nullptr;   // recorded after a ranker copied wsnap (otf_repo_rank_published)
 };
 
 namespace {
@@ -155,6 +163,29 @@ namespace {
 cudaStream_t pick_stream(cudaStream_t own, void* user) {
   (void)own;  // device-memory calls run on the caller's stream (NULL = legacy default stream)
   return static_cast<cudaStream_t>(user);
+}
+
+// Orders a call on stream st after the handle's previous call (whatever stream that used).
+int repo_enter(otf_repo* r, cudaStream_t st) {
+  if (r->used && r->last_stream != st) OTF_CUDA(cudaStreamWaitEvent(st, r->last, 0));
+  return OTF_OK;
+}
+// Records the end of this call's work on st (the next call on another stream waits for it).
+int repo_leave(otf_repo* r, cudaStream_t st) {
+  if (!r->last) OTF_CUDA(cudaEventCreateWithFlags(&r->last, cudaEventDisableTiming));
+  OTF_CUDA(cudaEventRecord(r->last, st));
+  r->last_stream = st;
+  r->used = true;
+  return OTF_OK;
+}
+// enter + body + leave (leave runs even when the body failed after enqueueing work)
+template <typename F>
+int repo_ordered(otf_repo* r, cudaStream_t st, F&& body) {
+  int rc = repo_enter(r, st);
+  if (rc) return rc;
+  rc = body();
+  const int rc2 = repo_leave(r, st);
+  return rc ? rc : rc2;
 }
 
 int make_stream(cudaStream_t* s, bool high_priority) {
@@ -169,13 +200,6 @@ int copy_in(void* dst, const void* src, size_t bytes, int mem, cudaStream_t st) 
   OTF_CUDA(cudaMemcpyAsync(dst, src, bytes,
                            mem == OTF_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                            st));
-  return OTF_OK;
-}
-
-int check_ids(const int64_t* ids, int64_t n, int mem) {
-  if (!ids || mem != OTF_MEM_HOST) return OTF_OK;
-  for (int64_t i = 0; i < n; ++i)
-    if (ids[i] < 0) return fail(OTF_ERR_CONFIG, "ids must be non-negative");
   return OTF_OK;
 }
 
@@ -194,8 +218,6 @@ int repo_common(otf_repo* r, int device, int64_t n, const int64_t* ids, int64_t 
                          (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
     cudaGetLastError();  // clear a failed query
     const int ids_mem = dev_ids ? OTF_MEM_DEVICE : OTF_MEM_HOST;
-    rc = check_ids(ids, n, ids_mem);
-    if (rc) return rc;
     OTF_CUDA(cudaMalloc(&r->ids, (size_t)(n > 0 ? n : 1) * sizeof(int64_t)));
     rc = copy_in(r->ids, ids, (size_t)n * sizeof(int64_t), ids_mem, r->stream);
     if (rc) return rc;
@@ -225,6 +247,7 @@ void repo_free(otf_repo* r) {
   if (r->owns_payload && r->payload) cudaFree(const_cast<void*>(r->payload));
   if (r->ids) cudaFree(r->ids);
   if (r->cents) cudaFree(r->cents);
+  if (r->last) cudaEventDestroy(r->last);
   r->w.release(); r->w32.release(); r->lut.release(); r->scores.release(); r->bins.release(); r->outbuf.release();
   r->multi.release(); r->wpub.release();
   r->h_w.release(); r->h_out.release();
@@ -439,8 +462,7 @@ int otf_repo_subset(const otf_repo* src_c, const int64_t* rows, int64_t n_keep, 
   if (!rc && cudaMalloc(&r->ids, (size_t)(n_keep > 0 ? n_keep : 1) * sizeof(int64_t)) != cudaSuccess)
     rc = cuda_fail(cudaGetLastError(), "cudaMalloc subset ids");
   // order the subset after any pending work on the source stream
-  if (!rc) { cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, src->stream); cudaStreamWaitEvent(r->stream, ev, 0); cudaEventDestroy(ev); }
+  if (!rc) rc = repo_enter(src, r->stream);
   if (!rc) rc = launch_gather_rows(static_cast<const uint8_t*>(src->payload), r->row_bytes,
                                    static_cast<const int64_t*>(d_rows.p), n_keep,
                                    static_cast<uint8_t*>(p), r->device, r->stream);
@@ -451,6 +473,7 @@ int otf_repo_subset(const otf_repo* src_c, const int64_t* rows, int64_t n_keep, 
     if (cudaMalloc(&r->cents, cb) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "cudaMalloc cents");
     if (!rc) rc = copy_in(r->cents, src->cents, cb, OTF_MEM_DEVICE, r->stream);
   }
+  if (!rc) rc = repo_leave(src, r->stream);
   if (!rc && cudaStreamSynchronize(r->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "subset");
   d_rows.release();
   if (rc) { repo_free(r); return rc; }
@@ -477,16 +500,19 @@ int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* strea
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
-  const double* dw = nullptr;
-  int rc = stage_w(r, w, mem, st, &dw);
-  if (rc) return rc;
-  const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
-  if (mem == OTF_MEM_DEVICE) return score_into(r, dw, out, nullptr, st);
-  if ((rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es))) return rc;
-  if ((rc = score_into(r, dw, r->scores.p, nullptr, st))) return rc;
-  OTF_CUDA(cudaMemcpyAsync(out, r->scores.p, (size_t)r->n * es, cudaMemcpyDeviceToHost, st));
-  OTF_CUDA(cudaStreamSynchronize(st));
-  return OTF_OK;
+  int rc = repo_ordered(r, st, [&]() -> int {
+    const double* dw = nullptr;
+    int rc = stage_w(r, w, mem, st, &dw);
+    if (rc) return rc;
+    const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
+    if (mem == OTF_MEM_DEVICE) return score_into(r, dw, out, nullptr, st);
+    if ((rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es))) return rc;
+    if ((rc = score_into(r, dw, r->scores.p, nullptr, st))) return rc;
+    OTF_CUDA(cudaMemcpyAsync(out, r->scores.p, (size_t)r->n * es, cudaMemcpyDeviceToHost, st));
+    return OTF_OK;
+  });
+  if (!rc && mem == OTF_MEM_HOST) OTF_CUDA(cudaStreamSynchronize(st));
+  return rc;
 }
 
 int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* stream) {
@@ -495,7 +521,8 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   if (!ms) return fail(OTF_ERR_CONFIG, "ms must not be NULL");
   cudaStream_t st = pick_stream(r->stream, stream);
   const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
-  int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
+  int rc = repo_enter(r, st);
+  if (!rc) rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
   if (!rc) rc = topk_ws_alloc(&r->topk, 1);
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
   const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
@@ -517,6 +544,8 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   cudaEventRecord(e1, st);
   if (!rc) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBinsMax * sizeof(uint32_t), st) == cudaSuccess
                     ? OTF_OK : cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
+  const int rc_leave = repo_leave(r, st);
+  if (!rc) rc = rc_leave;
   cudaError_t e = cudaEventSynchronize(e1);
   if (!rc && e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);
   cudaEventDestroy(e0);
@@ -538,10 +567,16 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
   if (out_n) *out_n = k_eff;
   if (k_eff == 0) return OTF_OK;
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
-  const double* dw = nullptr;
-  int rc = stage_w(r, w, mem, st, &dw);
+  if (mem == OTF_MEM_DEVICE)
+    return repo_ordered(r, st, [&]() -> int {
+      const double* dw = nullptr;
+      int rc = stage_w(r, w, mem, st, &dw);
+      return rc ? rc : rank_device(r, dw, k_eff, out_ids, out_scores, out_rows, st);
+    });
+  int rc = repo_enter(r, st);  // host mode: r->stream, synchronised below
   if (rc) return rc;
-  if (mem == OTF_MEM_DEVICE) return rank_device(r, dw, k_eff, out_ids, out_scores, out_rows, st);
+  const double* dw = nullptr;
+  if ((rc = stage_w(r, w, mem, st, &dw))) return rc;
   const size_t bytes = (size_t)k_eff * 24;
   if ((rc = r->outbuf.ensure(bytes))) return rc;
   if ((rc = r->h_out.ensure(bytes))) return rc;
@@ -550,8 +585,11 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
   // host calls replay the repository's cached graph of the query (staging and output buffers
   // are the handle's own, so the graph is reused by every host-memory rank of this k)
-  if ((rc = rank_graph_locked(r, dw, k_eff, d_ids, d_sc, d_rows, st))) return rc;
-  OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
+  rc = rank_graph_locked(r, dw, k_eff, d_ids, d_sc, d_rows, st);
+  if (!rc && cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync");
+  if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
+  if (rc) { cudaStreamSynchronize(st); return rc; }
   OTF_CUDA(cudaStreamSynchronize(st));
   const int64_t* h_ids = static_cast<const int64_t*>(r->h_out.p);
   std::memcpy(out_ids, h_ids, (size_t)k_eff * 8);
@@ -598,7 +636,8 @@ int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out,
     return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs dim % 32 == 0");
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
   const double* wp = W;
-  int rc = OTF_OK;
+  int rc = repo_enter(r, st);
+  if (rc) return rc;
   if (mem == OTF_MEM_HOST && (rc = stage_many(r, W, n_cls, st, &wp))) return rc;
   if (mem == OTF_MEM_HOST &&
       (rc = r->multi.ensure((size_t)std::min<int32_t>(n_cls, 64) * (r->n > 0 ? r->n : 1) * sizeof(float))))
@@ -613,6 +652,7 @@ int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out,
       if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
     }
   }
+  if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
   if (mem == OTF_MEM_HOST || rc) cudaStreamSynchronize(st);
   return rc;
 }
@@ -630,7 +670,8 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
   if (k_eff == 0) return OTF_OK;
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
   const double* wp = W;
-  int rc = OTF_OK;
+  int rc = repo_enter(r, st);
+  if (rc) return rc;
   const size_t lbytes = (size_t)n_cls * k_eff * 8;  // ids (int64) and scores (float64) per list entry
   if (mem == OTF_MEM_HOST) {
     if ((rc = stage_many(r, W, n_cls, st, &wp))) return rc;
@@ -654,6 +695,7 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
         rc = launch_topk(sbuf + (size_t)c * r->n, OTF_F32, r->n, r->ids, r->id_base, k_eff, &r->topk, false,
                          ids + (size_t)(c0 + c) * k_eff, sc + (size_t)(c0 + c) * k_eff, nullptr, r->device, st);
   }
+  if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
   if (!rc && mem == OTF_MEM_HOST) {
     // one D2H of both arrays into pinned staging, then plain copies into the caller's buffers
     cudaError_t e = cudaMemcpyAsync(r->h_out.p, r->outbuf.p, 2 * lbytes, cudaMemcpyDeviceToHost, st);
@@ -735,7 +777,8 @@ int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* id
   DeviceGuard g(r->device);
   int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
   if (k_eff == 0) return OTF_OK;
-  return rank_graph_locked(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, pick_stream(r->stream, stream));
+  cudaStream_t st = pick_stream(r->stream, stream);
+  return repo_ordered(r, st, [&]() { return rank_graph_locked(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, st); });
 }
 
 // ---- stateless primitives ----------------------------------------------------------------------
@@ -1132,8 +1175,10 @@ int otf_trainer_destroy(otf_trainer* t) {
   DeviceGuard g(t->device);
   if (t->stream) cudaStreamSynchronize(t->stream);
   t->w.release(); t->neg.release(); t->pos_pool.release(); t->pos_stage.release(); t->idx.release();
+  t->wsnap.release();
   t->h_stage.release(); t->h_idx.release();
   if (t->published) cudaEventDestroy(t->published);
+  if (t->consumed) cudaEventDestroy(t->consumed);
   if (t->stream) cudaStreamDestroy(t->stream);
   delete t;
   return OTF_OK;
@@ -1327,7 +1372,9 @@ int otf_group_rank(otf_group* g, otf_repo* r, const double* w, int32_t root, int
   int64_t* lid = reinterpret_cast<int64_t*>(lsc + k_eff);
   int64_t* lrow = lid + k_eff;
   const int64_t k_loc = std::min<int64_t>(k_eff, r->n);
-  if (k_loc > 0 && (rc = rank_device(r, dw, k_loc, lid, lsc, lrow, st))) return rc;
+  if (k_loc > 0 && (rc = repo_enter(r, st))) return rc;
+  if (k_loc > 0 && (rc = rank_device(r, dw, k_loc, lid, lsc, lrow, st))) { repo_leave(r, st); return rc; }
+  if (k_loc > 0 && (rc = repo_leave(r, st))) return rc;
   if ((rc = launch_group_finalize(lsc, lid, lrow, k_loc, k_eff, row_offset,
                                   (int64_t(1) << 62) + (int64_t)g->rank * k_eff, st)))
     return rc;
@@ -1442,6 +1489,9 @@ int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* 
 }
 
 // ---- snapshot publication: trainer w -> ranker buffer on the device (SURVEY.md §8b threading) ----
+// The snapshot lives in the TRAINER (t->wsnap), not in the repository: many sessions share one
+// repository (reference service.py:91, one WallRunner per session), so a publication must not be
+// overwritable by another session between its publish and its rank.
 int otf_trainer_publish(otf_trainer* t, otf_repo* r) {
   if (!t || !r) return fail(OTF_ERR_CONFIG, "trainer or repository is NULL");
   if (t->device != r->device) return fail(OTF_ERR_CONFIG, "trainer and repository are on different devices");
@@ -1449,40 +1499,55 @@ int otf_trainer_publish(otf_trainer* t, otf_repo* r) {
     return fail(OTF_ERR_CONFIG, "store dim " + std::to_string(r->model_dim) + " does not match model dim " +
                                     std::to_string(t->dim));
   std::lock_guard<std::mutex> lt(t->mu);
-  std::lock_guard<std::mutex> lr(r->mu);
   DeviceGuard g(t->device);
-  int rc = r->wpub.ensure((size_t)t->dim * 8);
+  int rc = t->wsnap.ensure((size_t)t->dim * 8);
   if (rc) return rc;
   if (!t->published) OTF_CUDA(cudaEventCreateWithFlags(&t->published, cudaEventDisableTiming));
   // the copy is ordered after every step already enqueued on the trainer stream and before any
-  // later one; the ranker's stream waits for it (no host round trip, no host copy of w)
-  OTF_CUDA(cudaMemcpyAsync(r->wpub.p, t->w.p, (size_t)t->dim * 8, cudaMemcpyDeviceToDevice, t->stream));
+  // later one, and after the last ranker's read of the previous snapshot (no host round trip)
+  if (t->consumed) OTF_CUDA(cudaStreamWaitEvent(t->stream, t->consumed, 0));
+  OTF_CUDA(cudaMemcpyAsync(t->wsnap.p, t->w.p, (size_t)t->dim * 8, cudaMemcpyDeviceToDevice, t->stream));
   OTF_CUDA(cudaEventRecord(t->published, t->stream));
-  OTF_CUDA(cudaStreamWaitEvent(r->stream, t->published, 0));
   return OTF_OK;
 }
 
-int otf_repo_rank_published(otf_repo* r, int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows,
-                            int64_t* out_n) {
-  if (!r) return fail(OTF_ERR_CONFIG, "repository is NULL");
+int otf_repo_rank_published(otf_repo* r, otf_trainer* t, int64_t k, int64_t* out_ids, double* out_scores,
+                            int64_t* out_rows, int64_t* out_n) {
+  if (!r || !t) return fail(OTF_ERR_CONFIG, "repository or trainer is NULL");
+  if (t->device != r->device) return fail(OTF_ERR_CONFIG, "trainer and repository are on different devices");
+  if (t->dim != r->model_dim)
+    return fail(OTF_ERR_CONFIG, "store dim " + std::to_string(r->model_dim) + " does not match model dim " +
+                                    std::to_string(t->dim));
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
-  if (!r->wpub.p || r->wpub.bytes < (size_t)r->model_dim * 8)
-    return fail(OTF_ERR_NOT_READY, "no snapshot published yet");
   int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
   if (out_n) *out_n = k_eff;
-  if (k_eff == 0) return OTF_OK;
   cudaStream_t st = r->stream;
   const size_t bytes = (size_t)k_eff * 24;
-  int rc = r->outbuf.ensure(bytes);
-  if (!rc) rc = r->h_out.ensure(bytes);
+  int rc = r->wpub.ensure((size_t)r->model_dim * 8);
+  if (!rc) rc = r->outbuf.ensure(bytes > 0 ? bytes : 8);
+  if (!rc) rc = r->h_out.ensure(bytes > 0 ? bytes : 8);
   if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> lt(t->mu);
+    if (!t->published) return fail(OTF_ERR_NOT_READY, "no snapshot published yet");
+    if (k_eff == 0) return OTF_OK;
+    // this trainer's snapshot -> the repository's ranking buffer, on the ranker's stream
+    if ((rc = repo_enter(r, st))) return rc;
+    OTF_CUDA(cudaStreamWaitEvent(st, t->published, 0));
+    OTF_CUDA(cudaMemcpyAsync(r->wpub.p, t->wsnap.p, (size_t)t->dim * 8, cudaMemcpyDeviceToDevice, st));
+    if (!t->consumed) OTF_CUDA(cudaEventCreateWithFlags(&t->consumed, cudaEventDisableTiming));
+    OTF_CUDA(cudaEventRecord(t->consumed, st));
+  }
   int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
   double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
   // the live ranker re-ranks every tau with a new w in the same buffer: one graph replay per tick
-  if ((rc = rank_graph_locked(r, static_cast<const double*>(r->wpub.p), k_eff, d_ids, d_sc, d_rows, st))) return rc;
-  OTF_CUDA(cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st));
+  rc = rank_graph_locked(r, static_cast<const double*>(r->wpub.p), k_eff, d_ids, d_sc, d_rows, st);
+  if (!rc && cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync");
+  if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
+  if (rc) { cudaStreamSynchronize(st); return rc; }
   OTF_CUDA(cudaStreamSynchronize(st));
   const int64_t* h = static_cast<const int64_t*>(r->h_out.p);
   std::memcpy(out_ids, h, (size_t)k_eff * 8);

@@ -78,6 +78,12 @@ __device__ __forceinline__ int64_t id_of(const int64_t* ids, int64_t id_base, in
   return ids ? ids[row] : id_base + row;
 }
 
+// Tie key of an id: larger inv <=> smaller (signed) id. Flipping the sign bit maps the signed
+// order onto the unsigned one, so negative ids (accepted by the reference) rank before positive
+// ones exactly as np.lexsort orders them.
+__device__ __forceinline__ uint64_t inv_id(int64_t id) { return ~((uint64_t)id ^ 0x8000000000000000ull); }
+__device__ __forceinline__ int64_t id_of_inv(uint64_t inv) { return (int64_t)(~inv ^ 0x8000000000000000ull); }
+
 __device__ __forceinline__ bool cand_greater(uint64_t ka, uint64_t ia, uint64_t kb, uint64_t ib) {
   return ka > kb || (ka == kb && ia > ib);
 }
@@ -320,7 +326,7 @@ __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0 && cnt < k_eff) {
-      out_ids[cnt] = (int64_t)~ii;
+      out_ids[cnt] = id_of_inv(ii);
       out_scores[cnt] = src.out_score(r, ki);
       if (out_rows) out_rows[cnt] = r;
     }
@@ -360,7 +366,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
       for (int64_t i = tid; i < n; i += nthreads) {
         const uint64_t key = score_key(__ldcg(scores + i));
         if (key == pre) {
-          const uint64_t inv = ~(uint64_t)id_of(ids, id_base, i);
+          const uint64_t inv = inv_id(id_of(ids, id_base, i));
           if ((inv & msk2) == pre2) atomicAdd(&h[(inv >> shift) & 255u], 1u);
         }
       }
@@ -400,7 +406,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
     if (i < n) {
       key = score_key(__ldcg(scores + i));
       const uint64_t mk = key & msk;
-      inv = ~(uint64_t)id_of(ids, id_base, i);
+      inv = inv_id(id_of(ids, id_base, i));
       in = mk > pre || (mk == pre && (!tie || (inv & msk2) >= pre2));
     }
     append_candidate(ws, in, key, inv, i, k_eff);
@@ -442,7 +448,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
   }
   for (int64_t t = tid; t < k_eff; t += nthreads) {
     const int64_t r = __ldcg(ws.row + t);
-    out_ids[t] = (int64_t)~__ldcg(ws.inv + t);
+    out_ids[t] = id_of_inv(__ldcg(ws.inv + t));
     out_scores[t] = src.out_score(r, __ldcg(ws.key + t));
     if (out_rows) out_rows[t] = r;
   }
@@ -621,7 +627,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
               const int64_t i = r0[j] + 32 * q + lane;
               if (slot < C) {
                 ws.key[slot] = score_key(src.exact(i, v[j][q]));
-                ws.inv[slot] = ~(uint64_t)id_of(ids, id_base, i);
+                ws.inv[slot] = inv_id(id_of(ids, id_base, i));
                 ws.row[slot] = i;
               }
               ++slot;
@@ -676,7 +682,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
             uint64_t key = 0, inv = 0;
             if (take) {
               key = score_key(src.exact(base + q, v[g][q]));
-              inv = ~(uint64_t)id_of(ids, id_base, base + q);
+              inv = inv_id(id_of(ids, id_base, base + q));
             }
             append_candidate(ws, take, key, inv, base + q, C);
           }

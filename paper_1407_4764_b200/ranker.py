@@ -340,19 +340,20 @@ class Repository:
             out.append(RankedList(ids[i].copy(), sc[i].copy(), model_version(m), produced_at, names))
         return out
 
-    def rank_published(self, k: int, produced_at: float = 0.0, model_version: int = 0) -> RankedList:
-        """rank(k) under the w an OnlineTrainer last published into this repository
-        (``OnlineTrainer.publish_to``): same list as ``rank(trainer.snapshot(), k)``."""
+    def rank_published(self, trainer, k: int, produced_at: float = 0.0, model_version: int = 0) -> RankedList:
+        """rank(k) under the w ``trainer`` last published (``OnlineTrainer.publish_to``): same
+        list as ``rank(trainer.snapshot(), k)``. The publication belongs to the trainer, so
+        sessions sharing this repository never rank under each other's weights."""
         n = self.count
         k_eff = max(0, min(int(k), n))
-        if k_eff == 0:
-            return _empty_list(model_version, produced_at, self.names)
         out_ids = np.empty(k_eff, dtype=np.int64)
         out_sc = np.empty(k_eff, dtype=np.float64)
         out_rows = np.empty(k_eff, dtype=np.int64) if self.names is not None else None
         got = C.c_int64(0)
-        _lib.check(_lib.load().otf_repo_rank_published(self._handle, k_eff, _lib.ptr(out_ids), _lib.ptr(out_sc),
-                                                       _lib.ptr(out_rows), C.byref(got)))
+        _lib.check(_lib.load().otf_repo_rank_published(self._handle, trainer.handle, k_eff, _lib.ptr(out_ids),
+                                                       _lib.ptr(out_sc), _lib.ptr(out_rows), C.byref(got)))
+        if k_eff == 0:
+            return _empty_list(model_version, produced_at, self.names)
         names = tuple(self.names[int(r)] for r in out_rows) if self.names is not None else None
         return RankedList(out_ids, out_sc, model_version, produced_at, names)
 

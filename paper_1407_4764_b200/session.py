@@ -6,14 +6,17 @@ semantically, with the state where the GPU needs it:
     training step gathers its B/2 positives on the device instead of converting the whole pool to
     float64 on the host every step (trainer.py:100-102);
   * ``train_step`` runs one Pegasos kernel on the trainer's high-priority stream;
-  * ``rank_tick`` publishes w from the trainer's buffer into the repository's ranking buffer on
-    the device (``OnlineTrainer.publish_to``: one device copy ordered on the trainer stream + a
-    CUDA event the ranker's stream waits on — no host round trip; versioned exactly like
-    trainer.py:161-173) and ranks the GPU-resident repository; the publication carries the same
-    CRC32 over the int64 ids / float64 scores bytes as session.py:96-116.
+  * ``rank_tick`` publishes w into the trainer's own snapshot buffer on the device
+    (``OnlineTrainer.publish_to``: one device copy ordered on the trainer stream + a CUDA event —
+    no host round trip; versioned exactly like trainer.py:161-173), then ranks the GPU-resident
+    repository under that snapshot (``Repository.rank_published(trainer, ...)``: the ranker's
+    stream waits for the event; the snapshot is per trainer, so sessions sharing a repository
+    never rank under each other's w); the publication carries the same CRC32 over the int64 ids /
+    float64 scores bytes as session.py:96-116.
 ``run_simulated`` replays a session on a virtual clock with the reference's event order
 (feeds at (i+1)/rate, training every 1/steps_per_second from the first arrival, rank ticks
-every interval; feed < train < rank at equal times — session.py:237-290).
+every interval; feed < train < rank at equal times — session.py:237-290). ``WallRunner`` is the
+wall-clock driver (session.py:295-359): feeder, trainer and ranker threads around one session.
 """
 
 from __future__ import annotations
@@ -21,6 +24,7 @@ from __future__ import annotations
 import dataclasses
 import heapq
 import threading
+import time
 import zlib
 
 import numpy as np
@@ -173,7 +177,8 @@ class QuerySession:
             _, version = self.trainer.publish_to(self.repository)
         except NotReadyError:
             return False
-        ranked = self.repository.rank_published(self.cfg.ranker.k, produced_at=now, model_version=version)
+        ranked = self.repository.rank_published(self.trainer, self.cfg.ranker.k, produced_at=now,
+                                                model_version=version)
         with self._lock:
             self._lists_published += 1
             pub = Publication.build(ranked, len(self.pool), self.trainer.iteration, self._lists_published)
@@ -229,3 +234,79 @@ def run_simulated(session: QuerySession, vectors, duration: float, on_publish=No
         elif session.rank_tick(at) and on_publish is not None:
             on_publish(session.latest_publication())
     session.mark_stopped(duration)
+
+
+class WallRunner:
+    """session.py:295-359 — the wall-clock driver: a feeder, a trainer and a ranker thread around
+    one session. Each role is a plain loop on the monotonic clock; ctypes releases the GIL inside
+    every library call, so the trainer's Pegasos kernels (high-priority stream) and the ranker's
+    scans overlap on the GPU. ``stop`` is idempotent and leaves the session stopped."""
+
+    def __init__(self, session: QuerySession, vectors):
+        self.session = session
+        self._vectors = np.asarray(vectors, dtype=np.float32)
+        self._halt = threading.Event()
+        roles = (("feeder", self._feed), ("trainer", self._train), ("ranker", self._rank))
+        self._threads = [threading.Thread(target=fn, name=f"{role}-{session.id}", daemon=True) for role, fn in roles]
+        self.errors: list[BaseException] = []
+
+    def start(self) -> None:
+        for th in self._threads:
+            th.start()
+
+    def stop(self) -> None:
+        self._halt.set()
+        me = threading.current_thread()
+        for th in self._threads:
+            if th is not me and th.ident is not None:
+                th.join(timeout=5.0)
+        self.session.mark_stopped(time.monotonic())
+
+    def _guard(self, body) -> None:
+        try:
+            body()
+        except BaseException as exc:  # a failing role fails the session, as a crashed thread would
+            self.errors.append(exc)
+            self.session.mark_failed(repr(exc), time.monotonic())
+            self._halt.set()
+
+    def _feed(self) -> None:
+        def body():
+            rate = self.session.cfg.rate
+            if rate <= 0:
+                return
+            t0 = time.monotonic()
+            for i, vec in enumerate(self._vectors):
+                wait = t0 + (i + 1) / rate - time.monotonic()
+                if (wait > 0 and self._halt.wait(wait)) or self._halt.is_set():
+                    return
+                self.session.feed_one(vec)
+        self._guard(body)
+
+    def _train(self) -> None:
+        def body():
+            gap = 1.0 / self.session.cfg.steps_per_second
+            while not self._halt.is_set():
+                t = time.monotonic()
+                if not self.session.train_step():
+                    self._halt.wait(0.005)
+                    continue
+                rest = gap - (time.monotonic() - t)
+                if rest > 0:
+                    self._halt.wait(rest)
+        self._guard(body)
+
+    def _rank(self) -> None:
+        def body():
+            interval = self.session.cfg.ranker.interval
+            due = time.monotonic() + interval
+            while True:
+                wait = due - time.monotonic()
+                if (wait > 0 and self._halt.wait(wait)) or self._halt.is_set():
+                    return
+                self.session.rank_tick(time.monotonic())
+                now = time.monotonic()
+                due += interval
+                if due < now:  # a slow tick skips the missed ticks instead of queueing them
+                    due = now + interval
+        self._guard(body)

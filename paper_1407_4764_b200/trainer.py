@@ -102,9 +102,11 @@ class OnlineTrainer:
             raise InsufficientDataError("negative pool must be a non-empty 2-D array")
         if neg.shape[1] != dim:
             raise ConfigError(f"negative pool dim {neg.shape[1]} does not match model dim {dim}")
-        # float64 pools keep their exact values (the reference converts pools to float64)
-        self._neg_dtype = _lib.F64 if neg.dtype == np.float64 else _lib.F32
-        neg = np.ascontiguousarray(neg, dtype=np.float64 if self._neg_dtype == _lib.F64 else np.float32)
+        # the reference stores OnlineTrainer negatives as float32 whatever their dtype
+        # (trainer.py:127: np.asarray(negatives, dtype=np.float32)); pegasos_step then widens the
+        # float32 rows to float64 exactly, which the kernel does per sampled row
+        self._neg_dtype = _lib.F32
+        neg = np.ascontiguousarray(neg, dtype=np.float32)
         self._dim = int(dim)
         self._n_neg = neg.shape[0]
         self._batch_hook = batch_hook

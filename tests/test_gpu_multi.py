@@ -104,6 +104,27 @@ def test_score_many_data_scales(otf, case):
         assert not np.all(np.isfinite(S[:, 17]))
 
 
+@pytest.mark.parametrize("scale", [1e7, 1e-7, 30.0])
+def test_score_many_mixed_row_magnitudes(otf, scale):
+    """Normalised rows plus one outlier row (x 1e7: every other row is 1e-7 of the largest
+    element; x 1e-7: one tiny row). The FP16 form's absolute error floor (~max|X| 2^-39.5 per
+    element) would break the per-row reference tolerance, so the repository must pick the TF32
+    form; a mild spread (x 30) keeps the FP16 form. Every row stays within 1e-6 |w| |x_row|."""
+    rng = np.random.default_rng(int(scale * 1000) % 977)
+    n, d, c = 2000, 512, 8
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    x[123] *= np.float32(scale)
+    W = rng.standard_normal((c, d))
+    S = otf.Repository.dense(otf.FeatureStore(x)).score_many(list(W))
+    ex = exact(x, W).T
+    xn = np.linalg.norm(x.astype(np.float64), axis=1)
+    for i in range(c):
+        tol = 1e-6 * np.linalg.norm(W[i]) * xn
+        err = np.abs(S[i].astype(np.float64) - ex[i])
+        assert np.all(err <= 0.25 * tol + np.spacing(np.abs(S[i]))), (i, float(np.max(err / tol)))
+
+
 def test_multi_errors(otf):
     repo = otf.Repository.dense(otf.FeatureStore(np.ones((10, 30), np.float32)))
     with pytest.raises(otf.ConfigError):

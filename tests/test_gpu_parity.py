@@ -198,6 +198,28 @@ def test_top_k_matches_oracle(otf, n, k, dtype, kind):
     np.testing.assert_array_equal(r.scores, o_sc)
 
 
+@pytest.mark.parametrize("n,k", [(5000, 700), (200_000, 1000), (20_000, 9000)])
+def test_top_k_signed_ids(otf, n, k):
+    """The reference accepts any int64 ids for top_k and Repository.quantized / binary; ties break
+    toward the smallest SIGNED id (np.lexsort), so negative ids come first."""
+    rng = np.random.default_rng(n + 3)
+    s = rng.integers(-3, 4, size=n).astype(np.float32)  # heavy ties: the id order decides
+    ids = rng.permutation(np.arange(-n, 2 * n, dtype=np.int64))[:n]
+    ids[:3] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max, -1]
+    r = otf.top_k(s, k, ids=ids)
+    o_ids, o_sc, _ = O.top_k(s, k, ids)
+    np.testing.assert_array_equal(r.ids, o_ids)
+    np.testing.assert_array_equal(r.scores, o_sc)
+    cents = rng.standard_normal((4, 16, 2)).astype(np.float32)
+    codes = rng.integers(0, 16, (n, 4), dtype=np.uint8)
+    w = rng.standard_normal(8)
+    pq = otf.Repository.quantized(otf.PQCodebook(cents), codes, ids=ids)
+    o_ids, o_sc, _ = O.top_k(O.score_pq(w, cents, codes), k, ids)
+    got = pq.rank(otf.LinearModel(w, 1, 1), k)
+    np.testing.assert_array_equal(got.ids, o_ids)
+    np.testing.assert_array_equal(got.scores, o_sc)
+
+
 def test_top_k_affine_invariance(otf):
     rng = np.random.default_rng(5)
     for _ in range(20):
@@ -392,6 +414,27 @@ def test_online_trainer_matches_reference(otf, golden):
     assert again.version == 60
     with pytest.raises(ValueError):
         again.weights[0] = 1.0
+
+
+def test_online_trainer_float64_negatives_are_stored_float32(otf, golden):
+    """trainer.py:127: OnlineTrainer keeps np.asarray(negatives, dtype=np.float32) whatever the
+    input dtype; pegasos_step then widens those float32 rows. float64 negatives that are not
+    float32-representable must follow the same trajectory as the reference (not their exact
+    float64 values)."""
+    import otf_oracle as O
+
+    pos, neg = golden["peg_pos"], golden["peg_neg"]
+    neg64 = neg.astype(np.float64) + np.random.default_rng(3).standard_normal(neg.shape) * 1e-5
+    assert not np.array_equal(neg64.astype(np.float32).astype(np.float64), neg64)
+    cfg = otf.TrainerConfig(lam=0.05, batch_size=16, seed=9)
+    tr = otf.OnlineTrainer(pos.shape[1], neg64, cfg)
+    rng = np.random.default_rng(9)
+    w = np.zeros(pos.shape[1])
+    neg_ref = neg64.astype(np.float32).astype(np.float64)
+    for t in range(1, 31):
+        tr.step(pos)
+        w = O.pegasos_step(w, t, pos.astype(np.float64), neg_ref, cfg.lam, cfg.batch_size, cfg.project, rng)
+        np.testing.assert_allclose(tr.snapshot().weights, w, rtol=1e-12, atol=1e-15)
 
 
 def test_online_trainer_device_pool_equals_host_pool(otf, golden):

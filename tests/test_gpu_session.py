@@ -55,14 +55,14 @@ def test_device_snapshot_publication_equals_host_snapshot(otf, golden):
     for _ in range(7):
         tr.step()
     it, ver = tr.publish_to(repo)
-    a = repo.rank_published(25, produced_at=1.5, model_version=ver)
+    a = repo.rank_published(tr, 25, produced_at=1.5, model_version=ver)
     snap = tr.snapshot()
     assert (snap.iteration, snap.version) == (it, ver)
     b = repo.rank(snap, 25, produced_at=1.5)
     assert list(a.ids) == list(b.ids) and np.array_equal(a.scores, b.scores)
     assert a.model_version == b.model_version == ver
     tr.step()  # a new iterate -> a new version; the published copy is unaffected until republished
-    c = repo.rank_published(25, model_version=ver)
+    c = repo.rank_published(tr, 25, model_version=ver)
     assert list(c.ids) == list(a.ids)
     it2, ver2 = tr.publish_to(repo)
     assert (it2, ver2) == (it + 1, ver + 1)
@@ -84,6 +84,6 @@ def test_published_and_host_ranks_interleave_across_k(otf, golden):
         tr.step()
         _, ver = tr.publish_to(repo)
         snap = tr.snapshot()
-        a = repo.rank_published(k, model_version=ver)
+        a = repo.rank_published(tr, k, model_version=ver)
         b = repo.rank(snap, k)
         assert list(a.ids) == list(b.ids) and np.array_equal(a.scores, b.scores), (step, k)
