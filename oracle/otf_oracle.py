@@ -338,3 +338,29 @@ def train_batch(pos, neg, c=0.25, batch_size=32, epochs=60, project=True, seed=0
                 best_obj, best_w = obj, w.copy()
     avg = tail / tail_len
     return (avg if hinge_objective(avg, feats, labels, lam) <= best_obj else best_w), total
+
+
+# ---------------------------------------------------------------------------------------------
+# synthetic corpora — store.py:243-362 (the BASELINE.json C1 workload)
+
+
+def generate_corpus_bundle(dim, classes, per_class, distractors, train_per_class, negative_count,
+                           seed=0, cluster_spread=0.1, center_spread=1.0):
+    """store.py:324-362: class centers, then train members (class by class), test members, the
+    test distractors and the negative pool, all from ONE default_rng(seed) in that order, each
+    store L2-normalised in float64 and cast to float32 (store.py:32-53). Returns
+    (train (classes*train_per_class, dim), test (classes*per_class + distractors, dim),
+    negatives (negative_count, dim)) float32; row r of a store has id r. Pinned by the CRC32s of
+    the real reference's stores in tests/golden/golden_c1.npz."""
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((classes, dim)) * center_spread
+
+    def members(n):
+        return [centers[c] + rng.standard_normal((n, dim)) * cluster_spread for c in range(classes)]
+
+    train = members(train_per_class)
+    test = members(per_class)
+    if distractors:
+        test.append(rng.standard_normal((distractors, dim)) * center_spread)
+    neg = rng.standard_normal((negative_count, dim)) * center_spread
+    return normalize_rows(np.vstack(train)), normalize_rows(np.vstack(test)), normalize_rows(neg)

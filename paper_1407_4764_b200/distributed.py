@@ -37,6 +37,21 @@ def shard_bounds(n_total: int, world: int, rank: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
+def pack_candidates(sc, ids, rows):
+    """3k int64 send block of one rank: float64 score bit patterns, then ids, then global rows."""
+    import torch
+
+    return torch.cat((sc.contiguous().view(torch.int64), ids.contiguous(), rows.contiguous()))
+
+
+def unpack_candidates(gathered, world: int):
+    """world*3k gathered blocks -> world*k float64 scores, ids, rows in rank order."""
+    import torch
+
+    g = gathered.view(world, 3, -1).transpose(0, 1).reshape(3, -1)
+    return g[0].contiguous().view(torch.float64), g[1].contiguous(), g[2].contiguous()
+
+
 class ShardBackend(Protocol):
     def to_device(self, arr: np.ndarray): ...
     def local_topk(self, w_dev, k: int): ...          # -> (scores f64[k], ids i64[k], rows i64[k]) padded
@@ -136,12 +151,12 @@ class ShardedRepository:
         sc, ids, rows = self.backend.local_topk(w_dev, k_eff)
         if world == 1:
             return sc[:k_eff], ids[:k_eff], rows[:k_eff]
-        all_sc = sc.new_empty(world * k_eff)
-        all_ids = ids.new_empty(world * k_eff)
-        all_rows = rows.new_empty(world * k_eff)
-        dist.all_gather_into_tensor(all_sc, sc.contiguous(), group=self.group)
-        dist.all_gather_into_tensor(all_ids, ids.contiguous(), group=self.group)
-        dist.all_gather_into_tensor(all_rows, rows.contiguous(), group=self.group)
+        # ONE all_gather of a packed 3k int64 block per rank: the float64 scores travel as
+        # their bit patterns next to the ids and global rows (one collective, not three)
+        packed = pack_candidates(sc, ids, rows)
+        gathered = packed.new_empty(world * packed.numel())
+        dist.all_gather_into_tensor(gathered, packed, group=self.group)
+        all_sc, all_ids, all_rows = unpack_candidates(gathered, world)
         return self.backend.merge_topk(all_sc, all_ids, all_rows, k_eff)
 
     def rank(self, model, k: int, produced_at: float = 0.0, root_only: bool = False) -> RankedList | None:

@@ -107,8 +107,11 @@ class PositivePool:
         vec = np.asarray(vector, dtype=np.float32)
         if vec.shape != (self._dim,):
             raise ConfigError(f"vector shape {vec.shape} does not match pool dim {self._dim}")
+        # the library call runs outside the pool lock: a feeder waiting for the GIL after the
+        # call must not hold the lock the trainer's snapshot() needs
+        n = self._trainer.append_positives(vec[np.newaxis, :])
         with self._lock:
-            self._count = self._trainer.append_positives(vec[np.newaxis, :])
+            self._count = max(self._count, n)
             return self._count
 
     def snapshot(self) -> PoolView:

@@ -112,6 +112,8 @@ class OnlineTrainer:
         self._batch_hook = batch_hook
         self._rng = np.random.default_rng(self.cfg.seed)
         self._lock = threading.Lock()
+        self._pool_lock = threading.Lock()
+        self._n_pos = 0
         self._iteration = 0
         self._version = 0
         self._published_iteration = -1
@@ -143,9 +145,11 @@ class OnlineTrainer:
             raise ConfigError(f"vector shape {arr.shape[1:]} does not match pool dim {self._dim}")
         _lib.check(_lib.load().otf_trainer_append_positives(self._handle, _lib.ptr(arr), _lib.F32, arr.shape[0],
                                                             _lib.MEM_HOST))
-        n = C.c_int64()
-        _lib.check(_lib.load().otf_trainer_pool_size(self._handle, C.byref(n)))
-        return n.value
+        # the pool size is tracked here, not read back: one library call (one GIL round trip)
+        # per append keeps the feeder cheap when a busy Python thread holds the GIL
+        with self._pool_lock:
+            self._n_pos += arr.shape[0]
+            return self._n_pos
 
     def step(self, positives=None) -> int:
         """trainer.py:145-159 — one update against the given (or the device) positive pool."""
@@ -156,9 +160,7 @@ class OnlineTrainer:
             pos = np.asarray(pos)
             n_pos = len(pos)
         else:
-            n = C.c_int64()
-            _lib.check(_lib.load().otf_trainer_pool_size(self._handle, C.byref(n)))
-            n_pos = n.value
+            n_pos = self._n_pos  # rows whose append has completed (the device pool holds them)
             pos = None
         if n_pos == 0:
             raise NotReadyError("no positives available yet")
