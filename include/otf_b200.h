@@ -69,7 +69,8 @@ typedef struct otf_repo otf_repo;
 /* Repository.dense(store) — ranker.py:176-178. data is (n, dim) float32 row-major.
  * ids: n int64 (NULL = id_base + row), in host or device memory (detected from the pointer,
  * independently of mem). If mem == OTF_MEM_DEVICE and borrow != 0 the handle reads `data` in
- * place (caller keeps it alive); otherwise it copies into its own HBM. */
+ * place (caller keeps it alive); otherwise it copies into its own HBM. A device payload is
+ * adopted after a device synchronisation (the caller's writes to it, on any stream, are done). */
 int otf_repo_create_dense(int device, const float* data, int64_t n, int32_t dim,
                           const int64_t* ids, int64_t id_base, int mem, int borrow,
                           otf_repo** out);
@@ -123,12 +124,16 @@ int otf_repo_score_many(otf_repo* repo, const double* W, int32_t n_cls, float* o
 int otf_repo_rank_many(otf_repo* repo, const double* W, int32_t n_cls, int64_t k, int64_t* out_ids,
                        double* out_scores, int64_t* out_n, int mem, void* stream);
 
+/* Diagnostics (no reference counterpart): how many PQ rank queries of this handle took the
+ * cut path's exact fallback (sampled threshold too high, or too many tied candidates). */
+int otf_repo_cut_fallbacks(otf_repo* repo, int64_t* out);
 /* Measurement hook (no reference counterpart; used by bench.py for the roofline): runs the
- * scoring kernel of otf_repo_rank exactly as rank does (PQ: the float32-screening bins scan; with
- * the fused histogram and chunk maxima) for a device-resident w on `stream`, times that kernel
+ * scoring kernel of otf_repo_rank(k) exactly as rank does (PQ: the cut scan for large n, else the
+ * float32-screening bins scan; with the fused histogram and chunk maxima) for a device-resident
+ * w on `stream`, times that kernel
  * with CUDA events recorded around its launch(es) on the same stream, and returns the elapsed
  * milliseconds in *ms (synchronises the stream; leaves the rank workspace clean). */
-int otf_repo_time_rank_scan(otf_repo* repo, const double* w_dev, float* ms, void* stream);
+int otf_repo_time_rank_scan(otf_repo* repo, const double* w_dev, int64_t k, float* ms, void* stream);
 
 /* Capture repo's rank(k) for a device-resident w into a CUDA graph and replay it
  * (the live ranker re-ranks every tau with a new w in the same buffer). Device memory only. */

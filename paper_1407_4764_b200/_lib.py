@@ -58,7 +58,8 @@ SIGNATURES: dict[str, list] = {
     "otf_repo_destroy": [_vp],
     "otf_repo_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64), _P(_i32)],
     "otf_repo_score": [_vp, _vp, _vp, _int, _vp],
-    "otf_repo_time_rank_scan": [_vp, _vp, _vp, _vp],
+    "otf_repo_time_rank_scan": [_vp, _vp, _i64, _vp, _vp],
+    "otf_repo_cut_fallbacks": [_vp, _P(_i64)],
     "otf_repo_rank": [_vp, _vp, _i64, _vp, _vp, _vp, _P(_i64), _int, _vp],
     "otf_repo_rank_graph": [_vp, _vp, _i64, _vp, _vp, _vp, _vp],
     "otf_repo_score_many": [_vp, _vp, _i32, _vp, _int, _vp],

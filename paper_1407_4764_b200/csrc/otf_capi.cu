@@ -128,7 +128,7 @@ struct otf_repo {
   // workspace that grew (e.g. a larger k) can never be replayed through a stale graph
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
-    const void* key[13] = {};
+    const void* key[14] = {};
     int64_t k = -1;
     int kernels = 0;  // kernels in the graph (launch accounting of each replay)
     uint64_t used = 0;
@@ -226,6 +226,9 @@ int repo_common(otf_repo* r, int device, int64_t n, const int64_t* ids, int64_t 
 }
 
 int take_payload(otf_repo* r, const void* data, size_t bytes, int mem, int borrow) {
+  // a device payload may still be being written by the caller's work on any stream (e.g. torch's
+  // legacy default stream, which the handle's non-blocking stream does not wait for): finish it
+  if (mem == OTF_MEM_DEVICE) OTF_CUDA(cudaDeviceSynchronize());
   if (mem == OTF_MEM_DEVICE && borrow) {
     r->payload = data;
     r->owns_payload = false;
@@ -308,6 +311,17 @@ int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, doub
   if (rc) return rc;
   if ((rc = topk_ws_alloc(&r->topk, k_eff))) return rc;
   const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
+  int cut_r = 0;
+  if (r->kind == OTF_KIND_PQ && pq_cut_plan(r->M, codes, r->n, k_eff, r->device, &cut_r)) {
+    // PQ cut path: LUT kernel, then one cooperative kernel that samples, streams the codes
+    // emitting only the rows that can reach the sampled threshold, and selects among them
+    if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas))) return rc;
+    if ((rc = topk_cut_alloc(&r->topk))) return rc;
+    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st, kCutLutReplicas)))
+      return rc;
+    return launch_pq_rank_cut(codes, r->n, static_cast<const double*>(r->lut.p), r->K, r->ids, r->id_base, k_eff,
+                              cut_r, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows, r->device, st);
+  }
   if (r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes)) {
     // PQ: the scan writes 2-byte bins, the top-k recomputes the candidates' exact scores
     if ((rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t)))) return rc;
@@ -515,7 +529,20 @@ int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* strea
   return rc;
 }
 
-int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* stream) {
+int otf_repo_cut_fallbacks(otf_repo* r, int64_t* out) {
+  if (!r || !out) return fail(OTF_ERR_CONFIG, "repository or out is NULL");
+  std::lock_guard<std::mutex> lk(r->mu);
+  DeviceGuard g(r->device);
+  *out = 0;
+  if (!r->topk.cut_word) return OTF_OK;
+  if (r->used) OTF_CUDA(cudaEventSynchronize(r->last));
+  unsigned int w = 0;
+  OTF_CUDA(cudaMemcpy(&w, r->topk.cut_word + 3, sizeof(w), cudaMemcpyDeviceToHost));
+  *out = w;
+  return OTF_OK;
+}
+
+int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* ms, void* stream) {
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   if (!ms) return fail(OTF_ERR_CONFIG, "ms must not be NULL");
@@ -526,7 +553,16 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   if (!rc) rc = topk_ws_alloc(&r->topk, 1);
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
   const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
-  const bool bins = r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes);
+  const int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
+  int cut_r = 0;
+  const bool cut = r->kind == OTF_KIND_PQ && pq_cut_plan(r->M, codes, r->n, k_eff, r->device, &cut_r);
+  const bool bins = !cut && r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes);
+  if (!rc && cut) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas);
+  if (!rc && cut) rc = topk_cut_alloc(&r->topk);
+  if (!rc && cut) rc = topk_ws_alloc(&r->topk, k_eff);
+  if (!rc && cut) rc = r->outbuf.ensure((size_t)(k_eff > 0 ? k_eff : 1) * 24);
+  if (!rc && cut)
+    rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st, kCutLutReplicas);
   if (!rc && bins) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t));
   if (!rc && bins) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
   if (!rc && bins) rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st);
@@ -536,13 +572,19 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, float* ms, void* s
   OTF_CUDA(cudaEventCreate(&e1));
   int clog = -1;
   cudaEventRecord(e0, st);
-  if (bins)
+  if (cut) {
+    // the fused kernel is the rank path's scoring kernel (scan + selection in one launch)
+    int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
+    rc = launch_pq_rank_cut(codes, r->n, static_cast<const double*>(r->lut.p), r->K, r->ids, r->id_base, k_eff, cut_r,
+                            &r->topk, static_cast<double*>(r->scores.p), d_ids, reinterpret_cast<double*>(d_ids + k_eff),
+                            d_ids + 2 * k_eff, r->device, st);
+  } else if (bins)
     rc = launch_pq_scan_bins(codes, r->n, static_cast<const double*>(r->lut.p), r->K,
                              static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st, r->topk.cmax, &clog);
   else
     rc = score_into(r, w_dev, r->scores.p, r->topk.hist, st, r->topk.cmax, &clog);
   cudaEventRecord(e1, st);
-  if (!rc) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBinsMax * sizeof(uint32_t), st) == cudaSuccess
+  if (!rc && !cut) rc = cudaMemsetAsync(r->topk.hist, 0, kHistBinsMax * sizeof(uint32_t), st) == cudaSuccess
                     ? OTF_OK : cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
   const int rc_leave = repo_leave(r, st);
   if (!rc) rc = rc_leave;
@@ -719,17 +761,18 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
   const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
   int rc = r->scores.ensure((size_t)(r->n > 0 ? r->n : 1) * es);
   if (!rc) rc = topk_ws_alloc(&r->topk, k_eff);
-  if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
+  if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas);
   if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
   if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
+  if (!rc && (r->kind == OTF_KIND_PQ)) rc = topk_cut_alloc(&r->topk);
   if (rc) return rc;
-  const void* key[13] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
-                         r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax};
+  const void* key[14] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
+                         r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax, r->topk.cut_key};
   otf_repo::GraphEntry* hit = nullptr;
   for (auto& ge : r->graphs) {
     bool same = ge.exec && ge.k == k_eff;
-    for (int i = 0; i < 13 && same; ++i) same = ge.key[i] == key[i];
+    for (int i = 0; i < 14 && same; ++i) same = ge.key[i] == key[i];
     if (same) { hit = &ge; break; }
   }
   if (!hit) {
@@ -760,7 +803,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
       cudaGraphExecDestroy(hit->exec);
     }
     hit->exec = exec;
-    for (int i = 0; i < 13; ++i) hit->key[i] = key[i];
+    for (int i = 0; i < 14; ++i) hit->key[i] = key[i];
     hit->k = k_eff;
     hit->kernels = kernels;
   }

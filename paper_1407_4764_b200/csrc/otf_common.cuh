@@ -82,7 +82,30 @@ __device__ __forceinline__ void hist_flush(const uint32_t* sh, uint32_t* g, int 
     if (sh[b]) atomicAdd(&g[b], sh[b]);
 }
 
-// Streaming 128-bit load that does not allocate in L1 (the dataset is read once per query).
+// Streaming 128-bit loads of the repository (read once per query): no L1 allocation, and an
+// L2 evict-first policy, so a 0.16-51 GB scan does not push the hot lines out of L2 every query
+// (the top-k kernel's code and workspaces, the LUT, the histogram, the candidate buffers).
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+#ifndef OTF_NO_EVICT_FIRST
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(l2_evict_first()));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(l2_evict_first()));
+  return r;
+}
+#else
 __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -97,6 +120,7 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
                : "l"(p));
   return r;
 }
+#endif
 
 __device__ __forceinline__ double shfl_xor_d(double v, int o) {
   return __shfl_xor_sync(0xffffffffu, v, o);

@@ -17,7 +17,8 @@ int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, fl
 
 // pq (otf_pq.cu)
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
-                  cudaStream_t st);
+                  cudaStream_t st, int replicas = 1);
+constexpr int kCutLutReplicas = 8;  // LUT copies the cut path's CTAs spread their reads over
 // pq_encode (pq.py:206-230): X (n, M*Q) f32, cents (M,K,Q) f32 -> codes (n, M) u8.
 size_t pq_encode_scratch_bytes(int M, int K);
 int launch_pq_encode(const float* X, int64_t n, int M, int K, int Q, const float* cents, void* scratch,
@@ -66,7 +67,19 @@ struct TopkWs {
   uint16_t* cmax = nullptr;
   size_t cmax_cap = 0;
   int clog = -1;
+  // PQ cut path (pq_scan16_cut -> topk_cut_kernel): the scan appends only the rows that can
+  // reach a sampled threshold. cut_word[0] = candidate count, [1] = the threshold's bin (both
+  // zero between calls); cut_smax: per-CTA sample maxima of the LUT/sample kernel.
+  uint64_t* cut_key = nullptr;    // (exact score order key, ~id) record per candidate (2 x cut_cap)
+  int64_t* cut_row = nullptr;     // row of each candidate
+  unsigned int* cut_word = nullptr;
+  uint32_t* cut_smax = nullptr;   // kCutSampleCtasMax entries
+  int64_t cut_cap = 0;
 };
+// candidate slots of the PQ cut path (16 B each); more candidates -> exact fallback
+constexpr int64_t kCutCap = 1 << 16;
+constexpr int kCutSampleCtasMax = 1024;
+int topk_cut_alloc(TopkWs* ws);
 // ensures ws->cmax holds the chunk maxima of n rows for chunks of >= 8 rows (zero padded)
 int topk_cmax_ensure(TopkWs* ws, int64_t n);
 int topk_ws_alloc(TopkWs* ws, int64_t k_eff, int n_seg = 1);
@@ -83,6 +96,15 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
 int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base,
                          int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores, int device,
                          cudaStream_t st);
+// PQ cut path (M == 16, large n): one cooperative kernel after the LUT kernel — samples the
+// score distribution, streams the codes emitting only the rows that can reach the sampled
+// threshold, and selects the exact top-k among them (or falls back to an exact select over every
+// row); see otf_pq.cu pq_rank_cut_kernel. pq_cut_plan returns r (the sample rank of the
+// threshold) or false when the path does not apply (small n or large k).
+bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int device, int* r);
+int launch_pq_rank_cut(const uint8_t* codes, int64_t n, const double* lut, int K, const int64_t* ids,
+                       int64_t id_base, int64_t k_eff, int r, TopkWs* ws, double* scratch, int64_t* out_ids,
+                       double* out_scores, int64_t* out_rows, int device, cudaStream_t st);
 int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,
                         int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, TopkWs* ws,
                         double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows,

@@ -21,6 +21,7 @@
 
 #include "otf_common.cuh"
 #include "otf_internal.h"
+#include "otf_topk_dev.cuh"
 
 namespace otf {
 
@@ -47,14 +48,17 @@ __device__ __forceinline__ double lut_entry_einsum(const float* __restrict__ c,
 }
 
 // lut is (M, K) row-major float64 (the reference's layout).
+// replicas > 1: copies r = 1.. at lut + r * M * K (the cut path's CTAs each read one copy, so
+// 148 SMs do not all hit the same 32 KB of L2 at once)
 __global__ void pq_build_lut_kernel(const float* __restrict__ cents, int M, int K, int Q,
-                                    const double* __restrict__ w, double* __restrict__ lut) {
+                                    const double* __restrict__ w, double* __restrict__ lut, int replicas) {
   // the dependent scan (programmatic launch) may start its own setup now
   asm volatile("griddepcontrol.launch_dependents;");
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= M * K) return;
   const int m = t / K;
-  lut[t] = lut_entry_einsum(cents + (int64_t)t * Q, w + (int64_t)m * Q, Q);
+  const double v = lut_entry_einsum(cents + (int64_t)t * Q, w + (int64_t)m * Q, Q);
+  for (int r = 0; r < replicas; ++r) lut[(int64_t)r * M * K + t] = v;
 }
 
 // numpy pairwise sum (n <= 128 branch and the recursive split), values from a getter.
@@ -219,9 +223,9 @@ __global__ void pq_check_codes(const uint8_t* __restrict__ codes, int64_t total,
 }
 
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
-                  cudaStream_t st) {
+                  cudaStream_t st, int replicas) {
   const int total = M * K;
-  pq_build_lut_kernel<<<(total + 255) / 256, 256, 0, st>>>(cents, M, K, Q, w, lut);
+  pq_build_lut_kernel<<<(total + 255) / 256, 256, 0, st>>>(cents, M, K, Q, w, lut, replicas);
   OTF_LAUNCH_CHECK("pq_build_lut");
   return OTF_OK;
 }
@@ -571,6 +575,580 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
     __syncthreads();
     hist_flush(sh, ghist, kPqHistBins);
   }
+}
+
+// ---- M == 16 cut path: one cooperative kernel (sampled threshold, candidate emission, select) ---
+// The rank path needs the k best rows, not every row's score. pq_rank_cut_kernel (one CTA per SM,
+// cooperative) streams the codes of its contiguous range of 2048-row chunks through shared
+// memory (1-D bulk copies, see below) and
+//   1. scores its FIRST chunk (a sample spread over the whole repository: one chunk per CTA) and
+//      publishes the sample's two largest screening scores; one grid barrier; every CTA takes
+//      T = the r-th largest of those 2 G values (r ~ 2 k_eff x sample / n, so ~2 k_eff rows
+//      are expected at or above T) and rounds it down to the lower edge of its 13-bit bin;
+//   2. keeps only the rows whose float32 screening score s32 can reach that edge (s32 >= T - 2
+//      eps, |s32 - s64| <= eps as in pq_scan16_f32bins): their exact float64 score (numpy's
+//      order, from the float64 LUT in shared memory) and row go to a candidate list and their
+//      exact bin to a histogram (global atomics: candidates are ~0.02% of the rows); nothing is
+//      written for the other rows (no per-row bins, no per-row histogram updates);
+//   3. one more grid barrier; every CTA finds the bin b0 of the k-th best candidate. All rows
+//      whose exact score lies in T's bin or above are candidates, so when b0 >= that bin the
+//      global top-k is among them: each CTA copies the candidates of bins >= b0 into its shared
+//      memory in list order (the same array in every CTA) and ranks its share by counting
+//      (candidate i on CTA i mod G), writing each to its output slot. Otherwise (T too high:
+//      fewer than k rows reached it, or more than kCutCap candidates: heavy ties, w = 0, a
+//      non-finite LUT) the kernel computes every row's exact score and runs the exact radix
+//      select (otf_topk_dev.cuh) — slower, same result.
+// Bit-exact with the reference either way (pq.py:248-276 scores, ranker.py:97-143 order).
+#ifdef OTF_CUT_TRACE  // diagnostic build (tools/gpu_cut_trace.sh): per-CTA globaltimer stamps
+#define CUT_STAMP(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[i]))
+#else
+#define CUT_STAMP(i)
+#endif
+
+__device__ __forceinline__ float key_to_f32(uint32_t k) {
+  return __uint_as_float((k >> 31) ? (k ^ 0x80000000u) : ~k);
+}
+
+// Rare: the lanes with emit bits append (exact float64 key, ~id) and the row of those rows
+// (warp-aggregated slot reservation). The record is self-contained, so the selection reads each
+// candidate once.
+template <int ROWS>
+__device__ __noinline__ void cut_emit(const unsigned char* sm, uint4 u0, uint4 u1, uint4 u2, uint4 u3, uint32_t emit,
+                                      int64_t row0, const int64_t* ids, int64_t id_base,
+                                      unsigned long long* cut_count, unsigned long long* cut_ge, uint64_t tkey64,
+                                      ulonglong2* cut_rec, int64_t* cut_row, int64_t cut_cap) {
+  static_assert(ROWS == 4, "four rows per lane");
+  const int lane = threadIdx.x & 31;
+  const uint4 uu[4] = {u0, u1, u2, u3};
+  uint32_t ge = 0;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const bool take = (emit >> i) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (bal == 0u) continue;
+    unsigned long long slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(cut_count, (unsigned long long)__popc(bal));
+    const int64_t slot = (int64_t)__shfl_sync(0xffffffffu, slot0, 0) + __popc(bal & ((1u << lane) - 1u));
+    // past the capacity only the count matters (the selection falls back)
+    if (take && slot < cut_cap) {
+      const uint32_t xw[4] = {uu[i].x, uu[i].y, uu[i].z, uu[i].w};
+      double a[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m)
+        a[m] = *reinterpret_cast<const double*>(sm + (((xw[m >> 2] >> (8 * (m & 3))) & 0xffu) << 8) + 8 * m);
+      double rr[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
+      const double ex = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                                  __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+      const int64_t row = row0 + 32 * i;
+      const uint64_t key = score_key(ex);
+      cut_rec[slot] = make_ulonglong2(key, inv_id(id_of(ids, id_base, row)));
+      cut_row[slot] = row;
+      ge |= (key >= tkey64) << i;
+    }
+  }
+  // candidates at or above T (the exact test the selection relies on), one atomic per warp
+  const unsigned n_ge = (unsigned)__popc(ge);
+  const unsigned tot = __reduce_add_sync(0xffffffffu, n_ge);
+  if (lane == 0 && tot) atomicAdd(cut_ge, (unsigned long long)tot);
+}
+
+// The codes stream through shared memory: 4096-row chunks (64 KB) land by 1-D bulk copies
+// (cp.async.bulk, the TMA engine) in a ring of kCutStages stages, each armed on an mbarrier with
+// its byte count (L2 evict-first: the repository is read once per query). CTA b owns a
+// contiguous range of chunks; its first stages are requested before griddepcontrol.wait (the
+// codes do not depend on the LUT kernel). Warp w scores rows [256 w, 256 w + 256) of a chunk in
+// two batches of 4 rows per lane (one conflict-free 16-byte shared load per row); the last warp
+// done with a stage refills it with the CTA's chunk kCutStages ahead.
+constexpr int kCutScanThreads = 512;  // 16 warps x 4 rows per lane (1024 x 2 and 1024 x 1 measured slower)
+constexpr int kCutRows = 4;           // rows per lane per batch
+constexpr int kCutBatches = 2;        // batches per warp per chunk
+constexpr int kCutStages = 2;
+constexpr int kCutBatchRows = kCutScanThreads * kCutRows;      // 2048 (the sample: batch 0 of chunk 0)
+constexpr int kCutChunkRows = kCutBatchRows * kCutBatches;      // 4096
+constexpr int kCutChunkBytes = kCutChunkRows * 16;
+
+__device__ __forceinline__ uint32_t cut_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// rows [r0, min(r0 + kCutChunkRows, end)) -> dst
+__device__ __forceinline__ void cut_issue(const uint8_t* codes, int64_t end, int64_t r0, unsigned char* dst,
+                                          uint64_t* bar, int64_t max_rows = kCutChunkRows) {
+  const int64_t rows = min(max_rows, end - r0);
+  const uint32_t bytes = (uint32_t)(rows * 16);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cut_smem_u32(bar)), "r"(bytes)
+               : "memory");
+#ifndef OTF_NO_EVICT_FIRST
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   cut_smem_u32(dst)),
+               "l"(codes + r0 * 16), "r"(bytes), "r"(cut_smem_u32(bar)), "l"(l2_evict_first())
+               : "memory");
+#else
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   cut_smem_u32(dst)),
+               "l"(codes + r0 * 16), "r"(bytes), "r"(cut_smem_u32(bar))
+               : "memory");
+#endif
+}
+
+__device__ __forceinline__ void cut_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(cut_smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+// Screening scores only (the sample chunk, before T is known).
+template <int ROWS>
+__device__ __forceinline__ void cut_scores(const unsigned char* sm, const uint4 (&u)[ROWS], const uint32_t (&kw)[8],
+                                           const uint32_t (&sel)[4], uint32_t s, float (&out)[ROWS]) {
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const uint32_t x0 = u[i].x, x1 = u[i].y, x2 = u[i].z, x3 = u[i].w;
+    const uint32_t t0 = sel_u32(s & 8, x2, x0), t1 = sel_u32(s & 8, x3, x1);
+    const uint32_t t2 = sel_u32(s & 8, x0, x2), t3 = sel_u32(s & 8, x1, x3);
+    const uint32_t wd[4] = {sel_u32(s & 4, t1, t0), sel_u32(s & 4, t0, t1), sel_u32(s & 4, t3, t2),
+                            sel_u32(s & 4, t2, t3)};
+    float b[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      b[t] = *reinterpret_cast<const float*>(sm + __byte_perm(wd[t >> 2], kw[t >> 1], sel[t & 3]));
+    uint64_t P[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) P[k] = pack_f2(b[2 * k], b[2 * k + 1]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) P[k] = fadd2(P[k], P[k + 4]);
+    P[0] = fadd2(P[0], P[2]);
+    P[1] = fadd2(P[1], P[3]);
+    P[0] = fadd2(P[0], P[1]);
+    out[i] = __fadd_rn(__uint_as_float((uint32_t)P[0]), __uint_as_float((uint32_t)(P[0] >> 32)));
+  }
+}
+
+// top two of a warp's (a >= b) pairs: returns (m1, m2) on every lane
+__device__ __forceinline__ void warp_top2(uint32_t a, uint32_t b, uint32_t& m1, uint32_t& m2) {
+  m1 = __reduce_max_sync(0xffffffffu, a);
+  const unsigned hit = __ballot_sync(0xffffffffu, a == m1);
+  const int first = __ffs(hit) - 1;
+  const uint32_t rest = ((int)(threadIdx.x & 31) == first) ? b : a;
+  m2 = __reduce_max_sync(0xffffffffu, rest);
+}
+
+constexpr size_t kRcSmem = 256 * 256 + (size_t)kCutStages * kCutChunkBytes;  // 192 KB
+constexpr int kRcCand = 4096;  // candidates the selection ranks in shared memory
+constexpr int kCutSelCtas = 1024;  // CTAs that select + rank (all: the ranking's shared traffic is ~C^2 / #CTAs)
+// selection layout in the (reused) dynamic shared memory: (key, inv) pairs, rows, 8192-bin histogram
+constexpr size_t kRcPairs = 0, kRcRows = (size_t)kRcCand * 16;
+static_assert(kRcRows + (size_t)kRcCand * 8 <= kRcSmem, "selection reuses the scan's shared memory");
+
+// max of four floats (emission test of a batch: one compare instead of four)
+__device__ __forceinline__ float max4(const float (&v)[4]) { return fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])); }
+
+__global__ void __launch_bounds__(kCutScanThreads, 1)
+pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* __restrict__ lut_g, int K,
+                   const int64_t* __restrict__ ids, int64_t id_base, int64_t k_eff, int r, TopkWs ws,
+                   double* __restrict__ scratch, int64_t* __restrict__ out_ids, double* __restrict__ out_scores,
+                   int64_t* __restrict__ out_rows) {
+  constexpr int ROWS = kCutRows;
+  // [256 LUT lines x 256 B][kCutStages x 64 KB code chunks]; the selection reuses all of it
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* stage = sm + 65536;
+  __shared__ __align__(8) uint64_t full[kCutStages];
+  __shared__ __align__(8) uint64_t sbar;  // the sample: the first half of chunk 0, requested first
+  __shared__ __align__(8) uint64_t lbar;  // the LUT replica (into the second half of stage 0)
+  __shared__ unsigned done[kCutStages];
+  __shared__ int64_t stage_chunk[kCutStages];  // chunk held by each stage (-1: none left)
+  __shared__ uint32_t smx[16];
+  __shared__ uint32_t s_top[2 * (kCutScanThreads / 32)];
+  __shared__ __align__(16) uint32_t s_all[kCutScanThreads];
+  __shared__ uint32_t s_tkey;
+  __shared__ uint32_t h[256];
+  __shared__ int s_b;
+  __shared__ int64_t s_above;
+  __shared__ unsigned s_wpre[33];
+  __shared__ unsigned s_last;
+#ifdef OTF_CUT_TRACE
+  unsigned long long ts[7] = {0, 0, 0, 0, 0, 0, 0};
+  CUT_STAMP(0);
+#endif
+  const unsigned G = gridDim.x, vb = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kCutScanThreads / 32;
+  // chunks of kCutChunkRows rows: CTA b's first chunk is c0 = floor(b nchunks / G) (the sample:
+  // spread over the whole repository, never the last, partial chunk); every other chunk is taken
+  // dynamically in row order from a global counter (skipping the G first chunks), so CTAs that
+  // stream faster take more chunks and all finish together
+  const int64_t nchunks = (n + kCutChunkRows - 1) / kCutChunkRows;  // >= 4 G (pq_cut_plan)
+  const int64_t c0 = (int64_t)vb * nchunks / G;
+  const int64_t rb = c0 * kCutChunkRows, re = n;  // rows of chunk c: [c * kCutChunkRows, min(+, n))
+  auto next_chunk = [&]() -> int64_t {  // the next dynamically assigned chunk, or -1
+    for (;;) {
+      const int64_t c = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(ws.cut_word + 8), 1ull);
+      if (c >= nchunks) return -1;
+      const int64_t b = (c * G + nchunks - 1) / nchunks;  // the only CTA whose c0 could be c
+      if (b >= (int64_t)G || b * nchunks / G != c) return c;
+    }
+  };
+  const uint32_t lut_bytes = (uint32_t)(16 * K * 8);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kCutStages; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&full[st])));
+      done[st] = 0u;
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&sbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&lbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the codes do not depend on the LUT kernel: the sample (batch 0 of chunk 0) and chunk 1
+    // stream in while it finishes
+    cut_issue(codes, re, rb, stage, &sbar, kCutBatchRows);
+    stage_chunk[0] = c0;
+    for (int st = 1; st < kCutStages; ++st) {
+      const int64_t c = next_chunk();
+      stage_chunk[st] = c;
+      if (c >= 0) cut_issue(codes, re, c * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
+      else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
+    }
+    s_tkey = 0u;
+  }
+  if (threadIdx.x < 16) smx[threadIdx.x] = 0u;
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the LUT: one bulk copy of this CTA's replica into the second half of stage 0, then
+  // rearranged into the lookup lines (entry (m, j) of the (M, K) table -> line j)
+  if (threadIdx.x == 0) {
+    const double* rep = lut_g + (int64_t)(vb % kCutLutReplicas) * 16 * K;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cut_smem_u32(&lbar)), "r"(lut_bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     cut_smem_u32(stage + kCutBatchRows * 16)),
+                 "l"(rep), "r"(lut_bytes), "r"(cut_smem_u32(&lbar))
+                 : "memory");
+  }
+  cut_wait(&lbar, 0u);
+  {
+    // 16 x 16 diagonal blocks per half-warp: lane l moves entry (m = l & 15, j = j0 + m) — the
+    // raw reads (bank 2 j) and the line writes (bank 2 m) are both conflict-free
+    const double* raw = reinterpret_cast<const double*>(stage + kCutBatchRows * 16);
+    const int m = lane & 15;
+    uint32_t mx = 0u;
+    for (int j0 = 2 * wid + (lane >> 4); j0 < 256; j0 += 2 * nw) {
+      const int jj = (j0 & ~15) | ((j0 + m) & 15);  // a permutation of the 16 j of the block
+      const double v = jj < K ? raw[m * K + jj] : 0.0;
+      unsigned char* line = sm + (jj << 8);
+      *reinterpret_cast<double*>(line + 8 * m) = v;
+      const float f = __double2float_rn(v);
+      *reinterpret_cast<float*>(line + 128 + 4 * m) = f;
+      *reinterpret_cast<float*>(line + 192 + 4 * m) = f;
+      mx = max(mx, __float_as_uint(fabsf(__double2float_ru(fabs(v)))));
+    }
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    if (lane < 16) atomicMax(&smx[m], mx);
+  }
+  __syncthreads();  // every read of the raw LUT is done: chunk 0's second half may land there
+  if (threadIdx.x == 0)
+    cut_issue(codes, re, rb + kCutBatchRows, stage + kCutBatchRows * 16, &full[0], kCutChunkRows - kCutBatchRows);
+  // (rows of c0 past n: the second half may be empty for a last partial chunk; pq_cut_plan keeps
+  // c0 + 1 <= nchunks - 1 so chunk c0 is full)
+  float eps;
+  bool screen;
+  {
+    double e = 0.0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) e += (double)__uint_as_float(smx[m]);
+    eps = __double2float_ru(e * 0x1p-20);
+    eps = fmaxf(eps, 0x1p-140f);
+    screen = e <= 1.0e38;
+  }
+  const uint32_t s = lane & 15;
+  uint32_t kw[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t c = 128u | ((uint32_t)(lane >> 4) << 6);
+    kw[u] = (c | (((uint32_t)(2 * u) ^ s) << 2)) | ((c | (((uint32_t)(2 * u + 1) ^ s) << 2)) << 8);
+  }
+  uint32_t sel[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sel[q] = 0x7604u | (uint32_t)(q & 1) | ((((uint32_t)q ^ s) & 3u) << 4);
+  unsigned long long* cut_count = reinterpret_cast<unsigned long long*>(ws.cut_word);
+  unsigned long long* cut_ge = reinterpret_cast<unsigned long long*>(ws.cut_word + 4);
+  ulonglong2* cut_rec = reinterpret_cast<ulonglong2*>(ws.cut_key);
+
+  // ---- 1. the sample: batch 0 of this CTA's first chunk ------------------------------------------
+  // batch bt of warp w: rows [bt * kCutBatchRows + 128 w, + 128) of the chunk
+  uint4 u0[ROWS];
+  float s0[ROWS];
+  const int64_t row00 = rb + wid * (32 * ROWS) + lane;
+  {
+    uint32_t ka = 0u, kb = 0u;  // this lane's two largest sample keys (0: below every key)
+    cut_wait(&sbar, 0u);
+    const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + wid * (32 * ROWS) + lane;
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) u0[i] = row00 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
+    cut_scores<ROWS>(sm, u0, kw, sel, s, s0);
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const uint32_t k = row00 + 32 * i < re ? (uint32_t)score_key(s0[i]) : 0u;
+      if (k > ka) { kb = ka; ka = k; } else if (k > kb) { kb = k; }
+    }
+    uint32_t m1, m2;
+    warp_top2(ka, kb, m1, m2);
+    if (lane == 0) { s_top[2 * wid] = m1; s_top[2 * wid + 1] = m2; }
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t v = lane < 2 * nw ? s_top[lane] : 0u;
+      uint32_t c1, c2;
+      warp_top2(v, 0u, c1, c2);
+      if (lane == 0) { ws.cut_smax[2 * vb] = c1; ws.cut_smax[2 * vb + 1] = c2; }
+    }
+  }
+  CUT_STAMP(1);
+  grid_barrier(ws.bar, G);
+  // T = the r-th largest of the 2 G sample maxima at 16-bit key resolution (two 8-bit radix
+  // passes in shared memory), rounded down to that key's lower edge
+  {
+    const int nv = 2 * (int)G;  // <= blockDim (pq_cut_plan)
+    const uint32_t v = (int)threadIdx.x < nv ? __ldcg(ws.cut_smax + threadIdx.x) : 0u;
+    const bool real = v != 0u;
+    uint32_t prefix = 0;
+    int64_t need = r;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int shift = 24 - 8 * pass;
+      if (threadIdx.x < 256) h[threadIdx.x] = 0u;
+      __syncthreads();
+      if (real && (pass == 0 || (v >> 24) == prefix)) atomicAdd(&h[(v >> shift) & 255u], 1u);
+      __syncthreads();
+      const int have = __syncthreads_count(real && (pass == 0 || (v >> 24) == prefix));
+      if (have < need) break;  // fewer than r sampled values (uniform)
+      pick_bin256(h, need, &s_b, &s_above);
+      __syncthreads();
+      need -= s_above;
+      prefix = pass == 0 ? (uint32_t)s_b : (prefix << 8) | (uint32_t)s_b;
+      if (pass == 1 && threadIdx.x == 0) s_tkey = prefix << 16;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  const uint32_t tkey = s_tkey;
+  const float T = key_to_f32(tkey);
+  // every row whose exact score x >= T has s32 >= x - eps >= T - eps: it is emitted
+  const float t_emit = __fsub_rd(T, eps);
+  const bool usable = screen && tkey != 0u && !isnan(t_emit) && !isinf(T);
+  const uint64_t tkey64 = score_key((double)T);
+  CUT_STAMP(2);
+
+  // ---- 2. emission: the held sample rows, then the rest of the range ------------------------------
+  if (usable && __any_sync(0xffffffffu, max4(s0) >= t_emit)) {
+    uint32_t emit = 0;
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i)
+      if (s0[i] >= t_emit && row00 + 32 * i < re) emit |= 1u << i;
+    cut_emit<ROWS>(sm, u0[0], u0[1], u0[2], u0[3], emit, row00, ids, id_base, cut_count, cut_ge, tkey64, cut_rec,
+                   ws.cut_row, ws.cut_cap);
+  }
+  for (int64_t j = 0;; ++j) {
+    const int st = (int)(j % kCutStages);
+    cut_wait(&full[st], (uint32_t)((j / kCutStages) & 1));  // (j == 0: the second half of chunk c0)
+    const int64_t c = stage_chunk[st];
+    if (c < 0) break;
+    const int64_t cr0 = c * kCutChunkRows;
+    const bool full_chunk = cr0 + kCutChunkRows <= re;
+#pragma unroll 1
+    for (int bt = (j == 0 ? 1 : 0); bt < kCutBatches; ++bt) {
+      const int off = bt * kCutBatchRows + wid * (32 * ROWS) + lane;
+      const uint4* rows4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + off;
+      const int64_t row0 = cr0 + off;
+      uint4 u[ROWS];
+      float sc[ROWS];
+      if (full_chunk) {
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) u[i] = rows4[32 * i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) u[i] = row0 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
+      }
+      if (!usable) continue;
+      cut_scores<ROWS>(sm, u, kw, sel, s, sc);
+      if (__any_sync(0xffffffffu, max4(sc) >= t_emit)) {
+        uint32_t emit = 0;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i)
+          if (sc[i] >= t_emit && row0 + 32 * i < re) emit |= 1u << i;
+        cut_emit<ROWS>(sm, u[0], u[1], u[2], u[3], emit, row0, ids, id_base, cut_count, cut_ge, tkey64, cut_rec,
+                       ws.cut_row, ws.cut_cap);
+      }
+    }
+    __syncwarp();  // this warp's reads of the stage are complete (consumed above)
+    if (lane == 0 && atomicAdd(&done[st], 1u) == (unsigned)(nw - 1)) {
+      done[st] = 0u;
+      const int64_t nc = next_chunk();
+      stage_chunk[st] = nc;  // published to the consumers by the barrier phase below
+      if (nc >= 0) cut_issue(codes, re, nc * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
+      else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
+    }
+  }
+  CUT_STAMP(3);
+  grid_barrier(ws.bar, G);  // every candidate record is in place
+  CUT_STAMP(4);
+
+  // ---- 3. selection ----------------------------------------------------------------------------
+  // Every row with exact score >= T is a candidate, so when at least k_eff candidates are >= T
+  // the global top-k is among those: the first kCutSelCtas CTAs copy them (list order, the same
+  // array in every CTA) into shared memory and rank them by counting. All CTAs decide the branch
+  // from the same two counters.
+  const unsigned long long c_all = __ldcg(cut_count), c_ge = __ldcg(cut_ge);
+  constexpr int kHeld = 8;  // records per thread: 4096 candidates
+  const bool ok = usable && c_all <= (unsigned long long)(kHeld * kCutScanThreads) && c_ge >= (unsigned long long)k_eff;
+  const unsigned gsel = min(G, (unsigned)kCutSelCtas);
+  // the last CTA done with the shared counters clears them for the next query
+  auto leave = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
+      if (s_last) { ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[4] = 0u; ws.cut_word[5] = 0u;
+                    ws.cut_word[8] = 0u; ws.cut_word[9] = 0u; ws.cut_word[6] = 0u; }
+    }
+  };
+  if (ok) {
+    if (vb >= gsel) { leave(); return; }
+    ulonglong2* pairs = reinterpret_cast<ulonglong2*>(sm + kRcPairs);
+    int64_t* prow = reinterpret_cast<int64_t*>(sm + kRcRows);
+    const int m = (int)c_all;
+    const int e0 = (int)threadIdx.x * kHeld;
+    const int mine = max(0, min(kHeld, m - e0));
+    ulonglong2 rec[kHeld];
+    int64_t rws[kHeld];
+#pragma unroll
+    for (int q = 0; q < kHeld; ++q) {
+      rec[q] = q < mine ? __ldcg(cut_rec + e0 + q) : make_ulonglong2(0ull, 0ull);
+      rws[q] = q < mine ? __ldcg(ws.cut_row + e0 + q) : 0;
+    }
+    int kept = 0;
+#pragma unroll
+    for (int q = 0; q < kHeld; ++q) kept += (q < mine && rec[q].x >= tkey64);
+    unsigned incl = (unsigned)kept;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wpre[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned y = lane < nw ? s_wpre[lane] : 0u;
+      unsigned x = y;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned z = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += z;
+      }
+      s_wpre[lane] = x - y;
+    }
+    __syncthreads();
+    int pos = (int)(s_wpre[wid] + incl - (unsigned)kept);
+#pragma unroll
+    for (int q = 0; q < kHeld; ++q)
+      if (q < mine && rec[q].x >= tkey64) {
+        pairs[pos] = rec[q];
+        prow[pos] = rws[q];
+        ++pos;
+      }
+    CUT_STAMP(5);
+    leave();
+    __syncthreads();
+    const int C = (int)c_ge;
+    // rank candidates i == vb (mod gsel): one warp per candidate counts who beats it
+    for (int q = (int)vb + wid * (int)gsel; q < C; q += nw * (int)gsel) {
+      const ulonglong2 ci = pairs[q];
+      int cnt = 0;
+#pragma unroll 4
+      for (int jj = lane; jj < C; jj += 32) {
+        const ulonglong2 cj = pairs[jj];
+        cnt += cand_greater(cj.x, cj.y, ci.x, ci.y);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (lane == 0 && cnt < k_eff) {
+        out_ids[cnt] = id_of_inv(ci.y);
+        out_scores[cnt] = key_to_f64(ci.x);
+        if (out_rows) out_rows[cnt] = prow[q];
+      }
+    }
+#ifdef OTF_CUT_TRACE
+    CUT_STAMP(6);
+    if (threadIdx.x == 0)
+      printf("cutT cta %d C_all %llu C %d sample %.2f threshold %.2f scan %.2f barrier %.2f select %.2f rank %.2f total %.2f\n",
+             (int)vb, c_all, C, (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3,
+             (ts[4] - ts[3]) * 1e-3, (ts[5] - ts[4]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[6] - ts[0]) * 1e-3);
+#endif
+    return;
+  }
+  // ---- fallback: exact scores of every row, then the exact radix select -------------------------
+  // (the LUT replica 0 in global memory is the float64 table the exact scores read)
+  __syncthreads();
+  PqCutSrc src{PqBinSrc{nullptr, codes, lut_g, 16, K}};
+  const int64_t nthreads = (int64_t)G * blockDim.x;
+  for (int64_t i = (int64_t)vb * blockDim.x + threadIdx.x; i < n; i += nthreads) scratch[i] = src.exact(i, 0u);
+  grid_barrier(ws.bar, G);
+  if (vb == 0 && threadIdx.x == 0) {
+    ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[4] = 0u; ws.cut_word[5] = 0u;
+    ws.cut_word[8] = 0u; ws.cut_word[9] = 0u;
+    ws.cut_word[3] += 1u;  // fallbacks taken (diagnostics: otf_repo_cut_fallbacks)
+  }
+  radix_select_emit(static_cast<const double*>(scratch), src, n, ids, id_base, k_eff, ws, k_eff >= n, sm, out_ids,
+                    out_scores, out_rows, h, &s_b, &s_above, vb, G);
+}
+
+bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int device, int* r) {
+  static const bool off = getenv("OTF_PQ_NO_CUT") != nullptr;  // A/B switch (tools/)
+  if (off || M != 16 || !pq_fast_path(M, codes) || k_eff <= 0) return false;
+  const int g = std::min(sm_count(device), kCutSampleCtasMax);
+  if (n < (int64_t)g * kCutChunkRows * 4) return false;  // >= 4 chunks per CTA
+  if (2 * g > kCutScanThreads) return false;              // one sample maximum per selecting thread
+  const int64_t S = (int64_t)g * kCutBatchRows;            // batch 0 of every CTA's first chunk
+  // ~2 k_eff + 128 rows are expected at or above the r-th largest of the S sampled scores (the
+  // r-th order statistic of the sample: relative spread ~1/sqrt(r), so fewer than k_eff rows or
+  // more than the 4096 candidate slots of the selection are both many sigmas away); the CTAs
+  // publish their top two, so r <= g / 2 keeps the estimate close to the true r-th sample
+  const int64_t rr = ((2 * k_eff + 128) * S + n - 1) / n;
+  if (rr > g / 2) return false;
+  *r = (int)std::max<int64_t>(rr, 1);
+  return true;
+}
+
+int launch_pq_rank_cut(const uint8_t* codes, int64_t n, const double* lut, int K, const int64_t* ids,
+                       int64_t id_base, int64_t k_eff, int r, TopkWs* ws, double* scratch, int64_t* out_ids,
+                       double* out_scores, int64_t* out_rows, int device, cudaStream_t st) {
+  auto fn = pq_rank_cut_kernel;
+  static bool configured[64] = {false};
+  if (!configured[device & 63]) {
+    OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRcSmem));
+    configured[device & 63] = true;
+  }
+  const int g = std::min(sm_count(device), kCutSampleCtasMax);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g);
+  cfg.blockDim = dim3(kCutScanThreads);
+  cfg.dynamicSmemBytes = kRcSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the LUT kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool no_pdl = getenv("OTF_PQ_NO_PDL") != nullptr;
+  cfg.numAttrs = no_pdl ? 1 : 2;
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, codes, n, lut, K, ids, id_base, k_eff, r, *ws, scratch, out_ids, out_scores,
+                              out_rows));
+  OTF_LAUNCH_CHECK("pq_rank_cut_kernel");
+  return OTF_OK;
 }
 
 bool pq_fast_path(int M, const uint8_t* codes) {
