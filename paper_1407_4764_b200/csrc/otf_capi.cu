@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -101,6 +102,19 @@ struct HostBuf {
 
 using namespace otf;
 
+// NVTX ranges around the public entry points (nvtx3 is header-only: a no-op unless a profiler
+// such as Nsight Systems injects itself), so a timeline shows which library call each kernel,
+// copy and synchronisation belongs to.
+#include <nvtx3/nvToolsExt.h>
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define OTF_NVTX(name) NvtxRange _otf_nvtx_range(name)
+
+
 struct otf_repo {
   int device = 0;
   int kind = OTF_KIND_DENSE;
@@ -128,7 +142,7 @@ struct otf_repo {
   // workspace that grew (e.g. a larger k) can never be replayed through a stale graph
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
-    const void* key[14] = {};
+    const void* key[16] = {};
     int64_t k = -1;
     int kernels = 0;  // kernels in the graph (launch accounting of each replay)
     uint64_t used = 0;
@@ -511,6 +525,7 @@ int otf_repo_info(const otf_repo* r, int32_t* kind, int64_t* count, int32_t* mod
 }
 
 int otf_repo_score(otf_repo* r, const double* w, void* out, int mem, void* stream) {
+  OTF_NVTX("otf_repo_score");
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   cudaStream_t st = mem == OTF_MEM_DEVICE ? pick_stream(r->stream, stream) : r->stream;
@@ -598,11 +613,12 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* 
 
 namespace {
 int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* ids_dev, double* scores_dev,
-                      int64_t* rows_dev, cudaStream_t st);
+                      int64_t* rows_dev, cudaStream_t st, const void* h_in = nullptr, void* h_out = nullptr);
 }  // namespace
 
 int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, double* out_scores,
                   int64_t* out_rows, int64_t* out_n, int mem, void* stream) {
+  OTF_NVTX("otf_repo_rank");
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
@@ -617,19 +633,24 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
     });
   int rc = repo_enter(r, st);  // host mode: r->stream, synchronised below
   if (rc) return rc;
-  const double* dw = nullptr;
-  if ((rc = stage_w(r, w, mem, st, &dw))) return rc;
+  const size_t wbytes = (size_t)r->model_dim * sizeof(double);
   const size_t bytes = (size_t)k_eff * 24;
+  if ((rc = r->w.ensure(wbytes))) return rc;
+  if ((rc = r->h_w.ensure(wbytes))) return rc;
   if ((rc = r->outbuf.ensure(bytes))) return rc;
   if ((rc = r->h_out.ensure(bytes))) return rc;
-  int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
+  std::memcpy(r->h_w.p, w, wbytes);  // the previous host call synchronised: the staging is free
+  // the selection writes the (ids, scores, rows) block straight into the pinned host buffer
+  // (mapped into the device address space): no D2H copy after the kernels
+  static const bool d2h_copy = getenv("OTF_HOST_D2H_COPY") != nullptr;  // A/B switch (tools/)
+  int64_t* d_ids = static_cast<int64_t*>(d2h_copy ? r->outbuf.p : r->h_out.p);
   double* d_sc = reinterpret_cast<double*>(d_ids + k_eff);
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_sc + k_eff);
-  // host calls replay the repository's cached graph of the query (staging and output buffers
-  // are the handle's own, so the graph is reused by every host-memory rank of this k)
-  rc = rank_graph_locked(r, dw, k_eff, d_ids, d_sc, d_rows, st);
-  if (!rc && cudaMemcpyAsync(r->h_out.p, r->outbuf.p, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-    rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync");
+  // host calls replay the repository's cached graph of the whole query: H2D of w from the
+  // pinned staging, the kernels (staging and output buffers are the handle's own, so the graph
+  // is reused by every host-memory rank of this k)
+  rc = rank_graph_locked(r, static_cast<const double*>(r->w.p), k_eff, d_ids, d_sc, d_rows, st, r->h_w.p,
+                         d2h_copy ? r->h_out.p : nullptr);
   if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
   if (rc) { cudaStreamSynchronize(st); return rc; }
   OTF_CUDA(cudaStreamSynchronize(st));
@@ -670,6 +691,7 @@ int multi_score_group(otf_repo* r, const double* dW, int cn, float* out, cudaStr
 }  // namespace
 
 int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out, int mem, void* stream) {
+  OTF_NVTX("otf_repo_score_many");
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   if (r->kind != OTF_KIND_DENSE) return fail(OTF_ERR_CONFIG, "multi-classifier scoring needs a dense repository");
@@ -701,6 +723,7 @@ int otf_repo_score_many(otf_repo* r, const double* W, int32_t n_cls, float* out,
 
 int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, int64_t* out_ids,
                        double* out_scores, int64_t* out_n, int mem, void* stream) {
+  OTF_NVTX("otf_repo_rank_many");
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   if (r->kind != OTF_KIND_DENSE) return fail(OTF_ERR_CONFIG, "multi-classifier ranking needs a dense repository");
@@ -754,8 +777,11 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
 namespace {
 // rank(k) for a device w through the repository's cached CUDA graph (captured on the first call
 // for a given (w, outputs, stream, k), replayed afterwards). Caller holds r->mu.
+// h_in / h_out (host-memory rank): the graph also holds the H2D copy of w from the pinned
+// staging buffer h_in and the D2H copy of the (ids, scores, rows) block to h_out, so a host query
+// is ONE graph launch (no separate copy calls between the kernels).
 int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* ids_dev, double* scores_dev,
-                      int64_t* rows_dev, cudaStream_t st) {
+                      int64_t* rows_dev, cudaStream_t st, const void* h_in, void* h_out) {
   constexpr size_t kGraphCache = 4;
   // allocate everything outside capture (no-ops once the workspaces are large enough)
   const size_t es = score_dtype(r) == OTF_F64 ? 8 : 4;
@@ -767,12 +793,13 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
   if (!rc && (r->kind == OTF_KIND_PQ)) rc = topk_cut_alloc(&r->topk);
   if (rc) return rc;
-  const void* key[14] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
-                         r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax, r->topk.cut_key};
+  const void* key[16] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
+                         r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax, r->topk.cut_key,
+                         h_in, h_out};
   otf_repo::GraphEntry* hit = nullptr;
   for (auto& ge : r->graphs) {
     bool same = ge.exec && ge.k == k_eff;
-    for (int i = 0; i < 14 && same; ++i) same = ge.key[i] == key[i];
+    for (int i = 0; i < 16 && same; ++i) same = ge.key[i] == key[i];
     if (same) { hit = &ge; break; }
   }
   if (!hit) {
@@ -781,7 +808,12 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     OTF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     OTF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     const int64_t l0 = g_launches.load();
-    rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
+    if (h_in && cudaMemcpyAsync(const_cast<double*>(w_dev), h_in, (size_t)r->model_dim * sizeof(double),
+                                cudaMemcpyHostToDevice, cap) != cudaSuccess)
+      rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync (graph H2D)");
+    if (!rc) rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
+    if (!rc && h_out && cudaMemcpyAsync(h_out, ids_dev, (size_t)k_eff * 24, cudaMemcpyDeviceToHost, cap) != cudaSuccess)
+      rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync (graph D2H)");
     const int kernels = (int)(g_launches.load() - l0);
     g_launches.fetch_sub(kernels);  // captured, not launched
     cudaGraph_t graph = nullptr;
@@ -803,7 +835,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
       cudaGraphExecDestroy(hit->exec);
     }
     hit->exec = exec;
-    for (int i = 0; i < 14; ++i) hit->key[i] = key[i];
+    for (int i = 0; i < 16; ++i) hit->key[i] = key[i];
     hit->k = k_eff;
     hit->kernels = kernels;
   }
@@ -816,6 +848,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
 
 int otf_repo_rank_graph(otf_repo* r, const double* w_dev, int64_t k, int64_t* ids_dev,
                         double* scores_dev, int64_t* rows_dev, void* stream) {
+  OTF_NVTX("otf_repo_rank_graph");
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
@@ -935,6 +968,7 @@ int otf_pq_score_codes(int device, const double* lut, int32_t M, int32_t K, cons
 
 int otf_score_binary(int device, const uint8_t* codes, int64_t n, int32_t output_bits,
                      const double* w, float* out, int mem, void* stream) {
+  OTF_NVTX("otf_score_binary");
   if (output_bits <= 0) return fail(OTF_ERR_CONFIG, "output_bits must be positive");
   STATELESS_BEGIN(device, mem, stream)
   const int row_bytes = (output_bits + 7) / 8;
@@ -1022,6 +1056,7 @@ CachedScratchBuf& cached_scratch(int device) {
 int otf_pq_encode(int device, const float* vectors, int64_t n, int32_t dim, const float* centroids,
                   int32_t num_blocks, int32_t num_centroids, int32_t subdim, uint8_t* out_codes, int mem,
                   void* stream) {
+  OTF_NVTX("otf_pq_encode");
   if (num_blocks <= 0 || num_centroids <= 0 || subdim <= 0) return fail(OTF_ERR_CONFIG, "bad codebook shape");
   if (num_centroids > 256) return fail(OTF_ERR_CONFIG, "num_centroids must fit a byte (<= 256)");
   if ((int64_t)dim != (int64_t)num_blocks * subdim)
@@ -1082,6 +1117,7 @@ CachedTopkWs& cached_topk_ws(int device) {
 int otf_top_k(int device, const void* scores, int32_t dtype, int64_t n, const int64_t* ids, int64_t k,
               int64_t* out_ids, double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
               void* stream) {
+  OTF_NVTX("otf_top_k");
   const int64_t k_eff = k < 0 ? 0 : (k > n ? n : k);
   if (out_n) *out_n = k_eff;
   if (k_eff == 0) return OTF_OK;
@@ -1161,6 +1197,7 @@ int otf_train_batch(int device, const void* features, int32_t dtype, int64_t n_p
                     int32_t d, const int64_t* idx, int64_t total, int32_t bs, int64_t spe,
                     int64_t tail_start, int64_t tail_len, double lam, int project, double* w_out,
                     double* obj_hist, int mem, void* stream) {
+  OTF_NVTX("otf_train_batch");
   if (n <= 0 || n_pos <= 0 || n_pos >= n) return fail(OTF_ERR_INSUFFICIENT, "both classes need at least one example");
   if (d <= 0 || bs <= 0 || spe <= 0 || total <= 0) return fail(OTF_ERR_CONFIG, "bad train_batch shape");
   STATELESS_BEGIN(device, mem, stream)
@@ -1261,6 +1298,7 @@ int otf_trainer_pool_size(const otf_trainer* t, int64_t* n_pos) {
 int otf_trainer_step(otf_trainer* t, const void* positives, int32_t pos_dtype, int64_t n_pos,
                      const int64_t* pos_idx, const int64_t* neg_idx, int32_t half, double shrink,
                      double eta_over_b, int project, double radius) {
+  OTF_NVTX("otf_trainer_step");
   std::lock_guard<std::mutex> lk(t->mu);
   DeviceGuard g(t->device);
   const int64_t pool = positives ? n_pos : t->n_pos;
@@ -1383,6 +1421,7 @@ int otf_group_destroy(otf_group* g) {
 int otf_group_rank(otf_group* g, otf_repo* r, const double* w, int32_t root, int64_t row_offset, int64_t total_rows,
                    int64_t k, int64_t* out_ids, double* out_scores, int64_t* out_rows, int64_t* out_n, int mem,
                    void* stream) {
+  OTF_NVTX("otf_group_rank");
   if (!g || !r) return fail(OTF_ERR_CONFIG, "group or shard is NULL");
   if (r->device != g->device) return fail(OTF_ERR_CONFIG, "shard and group are on different devices");
   if (root < 0 || root >= g->n_ranks) return fail(OTF_ERR_CONFIG, "root out of range");
@@ -1508,6 +1547,7 @@ int otf_kmeans_destroy(otf_kmeans* h) {
 }
 
 int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* counts, double* objective) {
+  OTF_NVTX("otf_kmeans_step");
   if (!h) return fail(OTF_ERR_CONFIG, "k-means handle is NULL");
   DeviceGuard g(h->device);
   const size_t cb = (size_t)h->k * h->dim * 8;
@@ -1536,6 +1576,7 @@ int otf_kmeans_step(otf_kmeans* h, double* centroids, int32_t* assign, int64_t* 
 // repository (reference service.py:91, one WallRunner per session), so a publication must not be
 // overwritable by another session between its publish and its rank.
 int otf_trainer_publish(otf_trainer* t, otf_repo* r) {
+  OTF_NVTX("otf_trainer_publish");
   if (!t || !r) return fail(OTF_ERR_CONFIG, "trainer or repository is NULL");
   if (t->device != r->device) return fail(OTF_ERR_CONFIG, "trainer and repository are on different devices");
   if (t->dim != r->model_dim)
@@ -1556,6 +1597,7 @@ int otf_trainer_publish(otf_trainer* t, otf_repo* r) {
 
 int otf_repo_rank_published(otf_repo* r, otf_trainer* t, int64_t k, int64_t* out_ids, double* out_scores,
                             int64_t* out_rows, int64_t* out_n) {
+  OTF_NVTX("otf_repo_rank_published");
   if (!r || !t) return fail(OTF_ERR_CONFIG, "repository or trainer is NULL");
   if (t->device != r->device) return fail(OTF_ERR_CONFIG, "trainer and repository are on different devices");
   if (t->dim != r->model_dim)

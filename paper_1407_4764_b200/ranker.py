@@ -364,14 +364,17 @@ class Repository:
         ver = model_version(model)
         if k_eff == 0:
             return _empty_list(ver, produced_at, self.names)
-        out_ids = np.empty(k_eff, dtype=np.int64)
-        out_sc = np.empty(k_eff, dtype=np.float64)
-        out_rows = np.empty(k_eff, dtype=np.int64) if self.names is not None else None
-        got = C.c_int64(0)
-        _lib.check(_lib.load().otf_repo_rank(self._handle, _lib.ptr(w), k_eff, _lib.ptr(out_ids), _lib.ptr(out_sc),
-                                             _lib.ptr(out_rows), C.byref(got), _lib.MEM_HOST, None))
-        names = tuple(self.names[int(r)] for r in out_rows) if self.names is not None else None
-        return RankedList(out_ids, out_sc, ver, produced_at, names)
+        # one (3, k) int64 block for ids, float64 score bits and rows: one allocation and one
+        # address lookup on the per-query path
+        block = np.empty((3, k_eff), dtype=np.int64)
+        base = block.__array_interface__["data"][0]
+        rc = _lib.load().otf_repo_rank(self._handle, w.__array_interface__["data"][0], k_eff, base, base + 8 * k_eff,
+                                       base + 16 * k_eff if self.names is not None else None, None, _lib.MEM_HOST,
+                                       None)
+        if rc:
+            _lib.check(rc)
+        names = tuple(self.names[int(r)] for r in block[2]) if self.names is not None else None
+        return RankedList(block[0], block[1].view(np.float64), ver, produced_at, names)
 
 
 __all__ = ["RankedList", "RankerConfig", "Repository", "score_dense", "score_pq", "score_binary", "top_k",
