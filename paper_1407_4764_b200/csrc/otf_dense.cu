@@ -19,8 +19,12 @@
 //
 // HBM roofline: 4*d bytes per row; 0.5 flop/byte. Loads are 128-bit, coalesced, streamed
 // past L1 (ld.global.nc.L1::no_allocate); the grid is persistent (a multiple of the 148 SMs).
+#include <algorithm>
+#include <cstdlib>
+
 #include "otf_common.cuh"
 #include "otf_internal.h"
+#include "otf_topk_dev.cuh"
 
 namespace otf {
 
@@ -34,8 +38,53 @@ __device__ __forceinline__ float chunk_dot(const float4 x, const float4 w) {
   return __fmaf_rn(x.w, w.w, s);
 }
 
-// Fast path: d == 128 * CPL. Each warp handles R rows per iteration, then a transposed
-// butterfly gives ~2 shuffles per row.
+// One warp iteration of the fast path: rows [r0, r0 + R) (d == 128 * CPL). Each warp handles R
+// rows per iteration, then a transposed butterfly gives ~2 shuffles per row. Returns the score
+// of row r0 + row_of_lane<R, 32>(lane) (meaningful on its writer lane when that row is < n).
+// Every fast-path kernel (scores, fused rank) scores through this one function, so a row's
+// score is the same bits whichever kernel or shard computed it.
+template <int CPL, int R>
+__device__ __forceinline__ float dense_iter(const float4* __restrict__ X4, int64_t n, int64_t r0,
+                                           const float4* wr, int lane) {
+  const int64_t row_f4 = 32 * CPL;  // float4 per row
+  constexpr int LB = CPL < 8 ? CPL : 8;  // float4 loads per row per batch
+  double p[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) p[i] = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < CPL; c0 += LB) {
+    float4 v[R][LB];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t row = r0 + i;
+#pragma unroll
+      for (int c = 0; c < LB; ++c) {
+        if (row < n) v[i][c] = ld_stream_f4(X4 + row * row_f4 + lane + 32 * (c0 + c));
+        else v[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      double acc = p[i];
+#pragma unroll
+      for (int c = 0; c < LB; ++c) {
+        acc = __dadd_rn(acc, (double)chunk_dot(v[i][c], wr[lane + 32 * (c0 + c)]));
+      }
+      p[i] = acc;
+    }
+  }
+  transposed_reduce<R, 32>(p, lane);
+  return __double2float_rn(p[0]);
+}
+
+template <int CPL>
+__device__ __forceinline__ void stage_w(const double* __restrict__ w, float4* wr) {
+  for (int t = threadIdx.x; t < 32 * CPL; t += blockDim.x)
+    wr[t] = make_float4(__double2float_rn(w[4 * t]), __double2float_rn(w[4 * t + 1]),
+                        __double2float_rn(w[4 * t + 2]), __double2float_rn(w[4 * t + 3]));
+}
+
+// Fast path: d == 128 * CPL, every row's score (+ the fused histogram / chunk maxima).
 template <int CPL, int R>
 __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restrict__ X, int64_t n,
                                                            const double* __restrict__ w,
@@ -45,48 +94,18 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
   const int lane = threadIdx.x & 31;
   __shared__ float4 wr[32 * CPL];
   __shared__ uint32_t sh[kHistBins];
-  for (int t = threadIdx.x; t < 32 * CPL; t += blockDim.x)
-    wr[t] = make_float4(__double2float_rn(w[4 * t]), __double2float_rn(w[4 * t + 1]),
-                        __double2float_rn(w[4 * t + 2]), __double2float_rn(w[4 * t + 3]));
+  stage_w<CPL>(w, wr);
   if (ghist) hist_zero(sh);
   __syncthreads();
-  const int64_t row_f4 = 32 * CPL;  // float4 per row
   const float4* X4 = reinterpret_cast<const float4*>(X);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  constexpr int LB = CPL < 8 ? CPL : 8;  // float4 loads per row per batch
   for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
-    double p[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) p[i] = 0.0;
-#pragma unroll
-    for (int c0 = 0; c0 < CPL; c0 += LB) {
-      float4 v[R][LB];
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int64_t row = r0 + i;
-#pragma unroll
-        for (int c = 0; c < LB; ++c) {
-          if (row < n) v[i][c] = ld_stream_f4(X4 + row * row_f4 + lane + 32 * (c0 + c));
-          else v[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        double acc = p[i];
-#pragma unroll
-        for (int c = 0; c < LB; ++c) {
-          acc = __dadd_rn(acc, (double)chunk_dot(v[i][c], wr[lane + 32 * (c0 + c)]));
-        }
-        p[i] = acc;
-      }
-    }
-    transposed_reduce<R, 32>(p, lane);
+    const float s = dense_iter<CPL, R>(X4, n, r0, wr, lane);
     bool writer;
     const int slot = row_of_lane<R, 32>(lane, &writer);
     const int64_t row = r0 + slot;
     const bool active = writer && row < n;
-    const float s = __double2float_rn(p[0]);
     if (active) out[row] = s;
     if (ghist) hist_add(sh, active, hist_bin(s));
     if (R > 1 && cmax) {  // the warp's R consecutive rows are one top-k chunk
@@ -98,6 +117,285 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
     __syncthreads();
     hist_flush(sh, ghist);
   }
+}
+
+// ---- fused rank (score + exact top-k in one cooperative launch) --------------------------------
+// The rank path needs the k best rows, not every row's score. dense_rank_cut (persistent grid,
+// 2 CTAs x 8 warps per SM, cooperative) works on groups of R rows (one warp iteration each):
+//   1. the sample: warp w scores the `sit` groups starting at group w * floor(ngroups / nwarp)
+//      (nwarp * sit * R rows spread over the whole repository), keeps those scores in `scratch`
+//      and the CTA publishes its four largest sample keys; a split grid barrier: while the other
+//      CTAs finish their sample, each warp scores its first scan group and holds the scores in
+//      registers (HBM stays busy); every CTA then takes T = the r-th largest of the 4 G published
+//      keys at 16-bit key resolution (r ~ (2 k + 128) x sample / n, so ~2 k + 128 rows are
+//      expected at or above T), rounded down to that key prefix's lower edge;
+//   2. the scan: warp w scores groups w, w + nwarp, ... (interleaved as dense_score_fast, the
+//      sample groups skipped) and appends (key, ~id, row) of every row with key >= T to a
+//      candidate list (warp-aggregated atomics; ~0.2% of the rows at k = 1000, 1M rows): no
+//      per-row score, histogram or chunk-maximum writes;
+//   3. one more grid barrier; when at least k and at most kDcSelCap rows reached T, the global top
+//      k is among them: every CTA copies the candidates' 32-bit keys into shared memory and ranks
+//      its share by counting (candidate i on CTA i mod G; ids and rows are read only for exact
+//      key ties), writing each straight to its output slot. Otherwise (heavy ties, w = 0, a sample
+//      far off the distribution) every row's score is written to `scratch` and the exact radix
+//      select (otf_topk_dev.cuh) runs — slower, same result.
+// Order: (score desc, id asc), -0.0 tied with +0.0, the row as the last tie key (ranker.py:97-143).
+// Measured (B200, same box): C2 (1M x 2048) 1167 vs 1180 us per query for scan + top-k kernel;
+// C1 (1M x 128) 101.0 vs 98.9 us — at 14 warp iterations per warp the scan's finishing spread
+// (51-66 us between CTAs) costs what the top-k kernel did, so d = 128 keeps the two-kernel path.
+constexpr int kDcThreads = 256;
+constexpr int kDcSelCap = 5120;  // candidates ranked in shared memory (32-bit keys)
+constexpr int kDcFallbackK = 1280;  // the radix fallback ranks k (key, inv) pairs in the same memory
+constexpr size_t kDcSmem = (size_t)kDcSelCap * 4 > (size_t)kDcFallbackK * 16 ? (size_t)kDcSelCap * 4
+                                                                              : (size_t)kDcFallbackK * 16;
+constexpr int kDcPub = 4;         // sample keys published per CTA
+constexpr int kDcPerThread = 8;   // published keys per thread in the T search (G <= 512)
+constexpr int kDcHold = 1;        // scan groups a warp scores while the grid synchronises
+#ifdef OTF_DCUT_TRACE  // diagnostic build: per-CTA globaltimer stamps of the phases
+#define DC_STAMP(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[i]))
+#else
+#define DC_STAMP(i)
+#endif
+
+template <int CPL, int R>
+__global__ void __launch_bounds__(kDcThreads, 2)
+dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict__ w,
+               const int64_t* __restrict__ ids, int64_t id_base, int64_t k_eff, int r, int sit, TopkWs ws,
+               float* __restrict__ scratch, int64_t* __restrict__ out_ids, double* __restrict__ out_scores,
+               int64_t* __restrict__ out_rows) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ float4 wr[32 * CPL];
+  __shared__ uint32_t h[256];
+  __shared__ int s_b;
+  __shared__ int64_t s_above;
+  __shared__ uint32_t s_tkey;
+  __shared__ unsigned s_nz;
+  __shared__ unsigned s_last;
+  __shared__ uint32_t s_top[2 * (kDcThreads / 32)];
+  __shared__ unsigned s_gen;
+#ifdef OTF_DCUT_TRACE
+  unsigned long long ts[7] = {0, 0, 0, 0, 0, 0, 0};
+#endif
+  DC_STAMP(0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned G = gridDim.x, vb = blockIdx.x;
+  stage_w<CPL>(w, wr);
+  if (threadIdx.x == 0) { s_tkey = 0u; s_nz = 0u; }
+  __syncthreads();
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ngroups = (n + R - 1) / R;
+  const int64_t gps = ngroups / nwarp;  // sample stride (>= sit: dense_cut_plan)
+  const int64_t gs0 = warp * gps;       // this warp's sample groups [gs0, gs0 + sit)
+  auto is_sample = [&](int64_t g) {
+    const int64_t q = g / gps;
+    return q < nwarp && g - q * gps < sit;
+  };
+  bool writer;
+  const int slot = row_of_lane<R, 32>(lane, &writer);
+  unsigned long long* cut_count = reinterpret_cast<unsigned long long*>(ws.cut_word);
+  ulonglong2* cut_rec = reinterpret_cast<ulonglong2*>(ws.cut_key);
+  uint32_t* key32 = reinterpret_cast<uint32_t*>(ws.key);  // compact keys of the first kDcSelCap candidates
+
+  // ---- 1. the sample ------------------------------------------------------------------------------
+  {
+    uint32_t ka = 0u, kb = 0u;  // this lane's two largest sample keys (0: none)
+    for (int64_t g = gs0; g < gs0 + sit; ++g) {
+      const float s = dense_iter<CPL, R>(X4, n, g * R, wr, lane);
+      const int64_t row = g * R + slot;
+      if (writer && row < n) {
+        scratch[row] = s;
+        const uint32_t k = (uint32_t)score_key(s);
+        if (k > ka) { kb = ka; ka = k; } else if (k > kb) { kb = k; }
+      }
+    }
+    uint32_t m1, m2;
+    warp_top2(ka, kb, m1, m2);
+    if (lane == 0) { s_top[2 * wid] = m1; s_top[2 * wid + 1] = m2; }
+    __syncthreads();
+    if (wid == 0) {  // the CTA's four largest of its warps' 16 published keys
+      uint32_t v = lane < 2 * (kDcThreads / 32) ? s_top[lane] : 0u;
+#pragma unroll
+      for (int q = 0; q < kDcPub; ++q) {
+        const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+        const unsigned hit = __ballot_sync(0xffffffffu, v == m);
+        if (lane == __ffs(hit) - 1) v = 0u;
+        if (lane == 0) ws.cut_smax[kDcPub * vb + q] = m;
+      }
+    }
+  }
+  DC_STAMP(1);
+  // split barrier: while the other CTAs finish their sample, each warp scores kDcHold groups of
+  // the scan and holds their scores in registers (HBM stays busy; no idle wait)
+  const unsigned gen = grid_arrive(ws.bar, G, &s_gen);
+  // the scan: warp w takes groups w, w + nwarp, ... (interleaved as dense_score_fast), skipping
+  // the sample groups
+  auto next_group = [&](int64_t g) {
+    while (g < ngroups && is_sample(g)) g += nwarp;
+    return g;
+  };
+  int64_t gcur = next_group(warp);
+  float held[kDcHold];
+  int64_t heldg[kDcHold];
+#pragma unroll
+  for (int h2 = 0; h2 < kDcHold; ++h2) {
+    heldg[h2] = gcur;
+    held[h2] = 0.f;
+    if (gcur < ngroups) {  // warp-uniform
+      held[h2] = dense_iter<CPL, R>(X4, n, gcur * R, wr, lane);
+      gcur = next_group(gcur + nwarp);
+    }
+  }
+  grid_wait(ws.bar, gen);
+  DC_STAMP(2);
+  // T = the r-th largest published key at 16-bit resolution (two 8-bit radix passes in shared
+  // memory over the kDcPub G values, held in registers: one L2 round trip), rounded down to that
+  // prefix's lower edge
+  {
+    const int nv = kDcPub * (int)G;  // <= kDcPerThread * blockDim (dense_cut_plan)
+    uint32_t v[kDcPerThread];
+#pragma unroll
+    for (int q = 0; q < kDcPerThread; ++q) {
+      const int i = (int)threadIdx.x + q * kDcThreads;
+      v[q] = i < nv ? __ldcg(ws.cut_smax + i) : 0u;
+    }
+    unsigned nz = 0;
+#pragma unroll
+    for (int q = 0; q < kDcPerThread; ++q) nz += v[q] != 0u;
+    if (nz) atomicAdd(&s_nz, nz);  // read after the pass-0 barriers below
+    uint32_t prefix = 0;
+    int64_t need = r;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int shift = 24 - 8 * pass;
+      h[threadIdx.x] = 0u;  // blockDim == 256
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kDcPerThread; ++q)
+        if (v[q] != 0u && (pass == 0 || (v[q] >> 24) == prefix)) atomicAdd(&h[(v[q] >> shift) & 255u], 1u);
+      __syncthreads();
+      if ((int64_t)s_nz < need) break;  // fewer than r sampled keys (uniform): fallback
+      pick_bin256(h, need, &s_b, &s_above);
+      __syncthreads();
+      need -= s_above;
+      prefix = pass == 0 ? (uint32_t)s_b : (prefix << 8) | (uint32_t)s_b;
+      if (pass == 1 && threadIdx.x == 0) s_tkey = prefix << 16;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  const uint32_t tkey = s_tkey;
+  const bool usable = tkey != 0u;
+
+  // ---- 2. emission: the sample rows, the held groups, then the rest of the scan ----------------------
+  auto emit = [&](bool take, float s, int64_t row) {
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (bal == 0u) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cut_count, (unsigned long long)__popc(bal));
+    const int64_t sl = (int64_t)__shfl_sync(0xffffffffu, base, 0) + __popc(bal & lanemask_lt());
+    if (take && sl < ws.cut_cap) {
+      const uint64_t key = score_key(s);
+      cut_rec[sl] = make_ulonglong2((key << 32) | (uint64_t)__float_as_uint(s), inv_id(id_of(ids, id_base, row)));
+      ws.cut_row[sl] = row;
+      if (sl < kDcSelCap) key32[sl] = (uint32_t)key;
+    }
+  };
+  for (int64_t g = gs0; g < gs0 + sit; ++g) {
+    const int64_t row = g * R + slot;
+    const bool own = writer && row < n;
+    const float s = own ? scratch[row] : 0.f;  // this lane's own write above
+    emit(usable && own && (uint32_t)score_key(s) >= tkey, s, row);
+  }
+#pragma unroll
+  for (int h2 = 0; h2 < kDcHold; ++h2) {
+    const int64_t row = heldg[h2] * R + slot;
+    const bool own = heldg[h2] < ngroups && writer && row < n;
+    if (usable) emit(own && (uint32_t)score_key(held[h2]) >= tkey, held[h2], row);
+    else if (own) scratch[row] = held[h2];  // the fallback needs every score
+  }
+  for (; gcur < ngroups; gcur = next_group(gcur + nwarp)) {  // warp-uniform
+    const float s = dense_iter<CPL, R>(X4, n, gcur * R, wr, lane);
+    const int64_t row = gcur * R + slot;
+    const bool own = writer && row < n;
+    if (usable) emit(own && (uint32_t)score_key(s) >= tkey, s, row);
+    else if (own) scratch[row] = s;
+  }
+  DC_STAMP(3);
+  grid_barrier(ws.bar, G);  // every candidate record is in place
+  DC_STAMP(4);
+
+  // ---- 3. selection -------------------------------------------------------------------------------
+  const unsigned long long c_all = __ldcg(cut_count);
+  const bool ok = usable && c_all >= (unsigned long long)k_eff && c_all <= (unsigned long long)kDcSelCap;
+  // the last CTA done with the counters clears them for the next query
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
+    if (s_last) {
+      ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[6] = 0u;
+    }
+  }
+  if (ok) {
+    uint32_t* sk = reinterpret_cast<uint32_t*>(dyn);
+    const int C = (int)c_all;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
+    __syncthreads();
+    DC_STAMP(5);
+    const int nw = blockDim.x >> 5;
+    for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
+      const uint32_t ki = sk[q];
+      int cnt = 0;
+      unsigned tie = 0;  // some lane saw another candidate with the same key
+#pragma unroll 8
+      for (int j = lane; j < C; j += 32) {
+        const uint32_t kj = sk[j];
+        cnt += kj > ki;
+        tie |= kj == ki && j != q;
+      }
+      if (__any_sync(0xffffffffu, tie)) {  // exact key ties: (~id desc, row asc) decides
+        const ulonglong2 ci = __ldcg(cut_rec + q);
+        const int64_t ri = __ldcg(ws.cut_row + q);
+        for (int j = lane; j < C; j += 32) {
+          if (sk[j] != ki || j == q) continue;
+          const uint64_t ij = __ldcg(&cut_rec[j].y);
+          cnt += ij > ci.y || (ij == ci.y && __ldcg(ws.cut_row + j) < ri);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (lane == 0 && cnt < k_eff) {
+        const ulonglong2 ci = __ldcg(cut_rec + q);
+        out_ids[cnt] = id_of_inv(ci.y);
+        out_scores[cnt] = (double)__uint_as_float((uint32_t)ci.x);
+        if (out_rows) out_rows[cnt] = __ldcg(ws.cut_row + q);
+      }
+    }
+#ifdef OTF_DCUT_TRACE
+    DC_STAMP(6);
+    if (threadIdx.x == 0)
+      printf("dcutT cta %d C %d sample %.2f barrier1 %.2f scan %.2f barrier2 %.2f select %.2f rank %.2f total %.2f\n",
+             (int)vb, C, (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3,
+             (ts[5] - ts[4]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[6] - ts[0]) * 1e-3);
+#endif
+    return;
+  }
+  if (usable) {  // the candidates cannot be used: every remaining row's score (static, interleaved)
+    for (int64_t g = warp; g < ngroups; g += nwarp) {
+      if (is_sample(g)) continue;  // warp-uniform
+      const float s = dense_iter<CPL, R>(X4, n, g * R, wr, lane);
+      const int64_t row = g * R + slot;
+      if (writer && row < n) scratch[row] = s;
+    }
+    grid_barrier(ws.bar, G);
+  }
+  // ---- fallback: the exact radix select over every row's score ---------------------------------------
+  if (vb == 0 && threadIdx.x == 0) ws.cut_word[3] += 1u;  // fallbacks taken (diagnostics)
+  DirectSrc<float> src{scratch};
+  radix_select_emit(static_cast<const float*>(scratch), src, n, ids, id_base, k_eff, ws, k_eff >= n, dyn, out_ids,
+                    out_scores, out_rows, h, &s_b, &s_above, vb, G);
 }
 
 // Generic path: any d (and any alignment). One warp per row, same canonical order.
@@ -151,6 +449,99 @@ static int launch_fast(const float* X, int64_t n, const double* w, float* out, u
   OTF_LAUNCH_CHECK("dense_score_fast");
   if (cmax && clog) *clog = R == 8 ? 3 : R == 16 ? 4 : 5;  // log2(R)
   return OTF_OK;
+}
+
+// ---- fused rank launch ---------------------------------------------------------------------------
+namespace {
+int dc_R(int cpl) { return cpl == 1 ? 32 : cpl == 2 ? 4 : cpl == 4 ? 2 : cpl == 16 ? 2 : 1; }
+
+template <int CPL, int R>
+int dc_grid(int device) {
+  static int per_sm[64] = {0};
+  if (!per_sm[device & 63]) {
+    auto fn = dense_rank_cut<CPL, R>;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDcSmem) != cudaSuccess)
+      return 0;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kDcThreads, kDcSmem) != cudaSuccess) return 0;
+    per_sm[device & 63] = b;
+  }
+  return per_sm[device & 63] * sm_count(device);
+}
+
+int dc_grid_of(int cpl, int device) {
+  switch (cpl) {
+    case 1: return dc_grid<1, 32>(device);
+    case 2: return dc_grid<2, 4>(device);
+    case 4: return dc_grid<4, 2>(device);
+    case 8: return dc_grid<8, 1>(device);
+    case 16: return dc_grid<16, 2>(device);
+    case 32: return dc_grid<32, 1>(device);
+    default: return 0;
+  }
+}
+
+template <int CPL, int R>
+int dc_launch(const float* X, int64_t n, const double* w, const int64_t* ids, int64_t id_base, int64_t k_eff,
+              const DenseCutPlan& pl, TopkWs* ws, float* scratch, int64_t* out_ids, double* out_scores,
+              int64_t* out_rows, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)pl.grid);
+  cfg.blockDim = dim3(kDcThreads);
+  cfg.dynamicSmemBytes = kDcSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, dense_rank_cut<CPL, R>, X, n, w, ids, id_base, k_eff, pl.r, pl.sit, *ws, scratch,
+                              out_ids, out_scores, out_rows));
+  OTF_LAUNCH_CHECK("dense_rank_cut");
+  return OTF_OK;
+}
+}  // namespace
+
+bool dense_cut_plan(int32_t d, const float* X, int64_t n, int64_t k_eff, int device, DenseCutPlan* pl) {
+  static const bool off = getenv("OTF_DENSE_NO_CUT") != nullptr;  // A/B switch (tools/)
+  if (off || k_eff <= 0 || d % 128 != 0 || (((uintptr_t)X) & 15) != 0) return false;
+  const int cpl = d / 128;
+  static const bool d128 = getenv("OTF_DENSE_CUT_D128") != nullptr;  // A/B switch (tools/)
+  if (cpl == 1 && !d128) return false;  // measured slower at d = 128 (see dense_rank_cut)
+  if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && cpl != 16 && cpl != 32) return false;
+  // ~2 k + 128 candidates are expected; their count must stay well inside the shared-memory cap
+  const int64_t want = 2 * k_eff + 128;
+  if (2 * want > kDcSelCap || k_eff > kDcFallbackK) return false;
+  const int grid = dc_grid_of(cpl, device);
+  if (grid <= 0) return false;
+  const int64_t nwarp = (int64_t)grid * (kDcThreads / 32), R = dc_R(cpl);
+  if ((int64_t)kDcPub * grid > (int64_t)kDcPerThread * kDcThreads || kDcPub * grid > kCutSmaxCap) return false;
+  // the sample: enough rows that the threshold is the ~64th-largest sampled key (relative spread
+  // of the candidate count ~1/8), at least one group per warp, at most a quarter of the rows
+  const int64_t s_target = (64 * n + want - 1) / want;
+  const int64_t sit = std::max<int64_t>(1, (s_target + nwarp * R - 1) / (nwarp * R));
+  const int64_t S = sit * nwarp * R;
+  if (4 * S > n || sit > ((n + R - 1) / R) / nwarp) return false;
+  const int64_t rr = (want * S + n - 1) / n;
+  if (rr > grid) return false;  // the four published keys per CTA must cover the top r
+  pl->grid = grid;
+  pl->sit = (int)sit;
+  pl->r = (int)std::max<int64_t>(rr, 1);
+  return true;
+}
+
+int launch_dense_rank_cut(const float* X, int64_t n, int32_t d, const double* w, const int64_t* ids,
+                          int64_t id_base, int64_t k_eff, const DenseCutPlan& pl, TopkWs* ws, float* scratch,
+                          int64_t* out_ids, double* out_scores, int64_t* out_rows, cudaStream_t st) {
+  switch (d / 128) {
+    case 1: return dc_launch<1, 32>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 2: return dc_launch<2, 4>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 4: return dc_launch<4, 2>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 8: return dc_launch<8, 1>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 16: return dc_launch<16, 2>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 32: return dc_launch<32, 1>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    default: return fail(OTF_ERR_CONFIG, "dense_rank_cut: unsupported dimension");
+  }
 }
 
 // Scores n rows against the float64 model w (cast to float32 in-kernel). Pointers must be

@@ -15,6 +15,20 @@ int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, fl
                        uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax = nullptr,
                        int* clog = nullptr);
 
+// fused dense rank (score + exact top-k, one cooperative launch; otf_dense.cu dense_rank_cut).
+// dense_cut_plan returns false when the path does not apply (unaligned / unsupported d, large k,
+// a repository too small for the sample); then score + launch_topk run as before.
+struct TopkWs;
+struct DenseCutPlan {
+  int grid = 0;  // CTAs (all co-resident)
+  int sit = 0;   // sample groups per warp
+  int r = 0;     // sample rank of the threshold
+};
+bool dense_cut_plan(int32_t d, const float* X, int64_t n, int64_t k_eff, int device, DenseCutPlan* pl);
+int launch_dense_rank_cut(const float* X, int64_t n, int32_t d, const double* w, const int64_t* ids,
+                          int64_t id_base, int64_t k_eff, const DenseCutPlan& pl, TopkWs* ws, float* scratch,
+                          int64_t* out_ids, double* out_scores, int64_t* out_rows, cudaStream_t st);
+
 // pq (otf_pq.cu)
 int launch_pq_lut(const float* cents, int M, int K, int Q, const double* w, double* lut,
                   cudaStream_t st, int replicas = 1);
@@ -73,12 +87,13 @@ struct TopkWs {
   uint64_t* cut_key = nullptr;    // (exact score order key, ~id) record per candidate (2 x cut_cap)
   int64_t* cut_row = nullptr;     // row of each candidate
   unsigned int* cut_word = nullptr;
-  uint32_t* cut_smax = nullptr;   // kCutSampleCtasMax entries
+  uint32_t* cut_smax = nullptr;   // kCutSmaxCap entries (two sample maxima per CTA / warp)
   int64_t cut_cap = 0;
 };
 // candidate slots of the PQ cut path (16 B each); more candidates -> exact fallback
 constexpr int64_t kCutCap = 1 << 16;
 constexpr int kCutSampleCtasMax = 1024;
+constexpr int kCutSmaxCap = 16384;
 int topk_cut_alloc(TopkWs* ws);
 // ensures ws->cmax holds the chunk maxima of n rows for chunks of >= 8 rows (zero padded)
 int topk_cmax_ensure(TopkWs* ws, int64_t n);

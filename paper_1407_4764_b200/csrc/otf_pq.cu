@@ -732,15 +732,6 @@ __device__ __forceinline__ void cut_scores(const unsigned char* sm, const uint4 
   }
 }
 
-// top two of a warp's (a >= b) pairs: returns (m1, m2) on every lane
-__device__ __forceinline__ void warp_top2(uint32_t a, uint32_t b, uint32_t& m1, uint32_t& m2) {
-  m1 = __reduce_max_sync(0xffffffffu, a);
-  const unsigned hit = __ballot_sync(0xffffffffu, a == m1);
-  const int first = __ffs(hit) - 1;
-  const uint32_t rest = ((int)(threadIdx.x & 31) == first) ? b : a;
-  m2 = __reduce_max_sync(0xffffffffu, rest);
-}
-
 constexpr size_t kRcSmem = 256 * 256 + (size_t)kCutStages * kCutChunkBytes;  // 192 KB
 constexpr int kRcCand = 4096;  // candidates the selection ranks in shared memory
 constexpr int kCutSelCtas = 1024;  // CTAs that select + rank (all: the ranking's shared traffic is ~C^2 / #CTAs)

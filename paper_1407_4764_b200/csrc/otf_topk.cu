@@ -313,7 +313,7 @@ int topk_cut_alloc(TopkWs* ws) {
   OTF_CUDA(cudaMalloc(&ws->cut_row, kCutCap * sizeof(int64_t)));
   OTF_CUDA(cudaMalloc(&ws->cut_word, 16 * sizeof(unsigned int)));
   OTF_CUDA(cudaMemset(ws->cut_word, 0, 16 * sizeof(unsigned int)));
-  OTF_CUDA(cudaMalloc(&ws->cut_smax, kCutSampleCtasMax * sizeof(uint32_t)));
+  OTF_CUDA(cudaMalloc(&ws->cut_smax, kCutSmaxCap * sizeof(uint32_t)));
   ws->cut_cap = kCutCap;
   return OTF_OK;
 }

@@ -35,6 +35,30 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
   __syncthreads();
 }
 
+// Split grid barrier (same word as grid_barrier): arrive, do independent work, then wait.
+// grid_arrive returns the generation to wait on (every thread of the CTA gets it).
+__device__ __forceinline__ unsigned int grid_arrive(unsigned int* bar, unsigned int nblocks, unsigned int* s_gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
+    __threadfence();
+    const unsigned long long old = atomicAdd(word, 1ull);
+    *s_gen = (unsigned int)(old >> 32);
+    if ((unsigned int)old == nblocks - 1) atomicAdd(word, (1ull << 32) - nblocks);
+  }
+  __syncthreads();
+  return *s_gen;
+}
+__device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = bar + 1;
+    while (*vgen == gen) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int64_t id_of(const int64_t* ids, int64_t id_base, int64_t row) {
   return ids ? ids[row] : id_base + row;
 }
@@ -59,6 +83,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 __device__ __forceinline__ double key_to_f64(uint64_t k) {
   const uint64_t u = (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
   return __longlong_as_double((long long)u);
+}
+
+// top two of a warp's (a >= b) pairs: returns (m1, m2) on every lane
+__device__ __forceinline__ void warp_top2(uint32_t a, uint32_t b, uint32_t& m1, uint32_t& m2) {
+  m1 = __reduce_max_sync(0xffffffffu, a);
+  const unsigned hit = __ballot_sync(0xffffffffu, a == m1);
+  const int first = __ffs(hit) - 1;
+  const uint32_t rest = ((int)(threadIdx.x & 31) == first) ? b : a;
+  m2 = __reduce_max_sync(0xffffffffu, rest);
 }
 
 // ---- score sources ---------------------------------------------------------------------------

@@ -367,8 +367,8 @@ class Repository:
         # one (3, k) int64 block for ids, float64 score bits and rows: one allocation and one
         # address lookup on the per-query path
         block = np.empty((3, k_eff), dtype=np.int64)
-        base = block.__array_interface__["data"][0]
-        rc = _lib.load().otf_repo_rank(self._handle, w.__array_interface__["data"][0], k_eff, base, base + 8 * k_eff,
+        base = _lib.ptr(block)
+        rc = _lib.load().otf_repo_rank(self._handle, _lib.ptr(w), k_eff, base, base + 8 * k_eff,
                                        base + 16 * k_eff if self.names is not None else None, None, _lib.MEM_HOST,
                                        None)
         if rc:

@@ -58,7 +58,8 @@ def main(rep, out):
             rec["dram_bytes_total"] = rec["dram_bytes_read"] + rec.get("dram_bytes_write", 0.0)
         launches.append(rec)
     summary = {"source": rep, "launches": launches}
-    names = ("dense_score", "pq_scan", "bin_score", "multi_score", "pq_encode_kernel", "pq_encode_mma")
+    names = ("dense_rank_cut", "pq_rank_cut", "dense_score", "pq_scan", "bin_score", "multi_score", "pq_encode_kernel",
+             "pq_encode_mma")
     score = [l for l in launches if any(s in l["kernel"] for s in names)]
     if score:
         summary["dram_bytes_per_launch"] = score[0].get("dram_bytes_total")
