@@ -120,6 +120,165 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
   }
 }
 
+// Multi-slice rows (2048-8192 bits) in ONE launch: a cluster of S = RB / 128 CTAs, one slice per
+// CTA (each holds its slice's 128 KB byte table), all S CTAs on the same rows. Warp w of CTA s
+// scores its slice of 32 rows exactly as bin_score_bytes does; the float32 slice sums then meet
+// over distributed shared memory instead of a float64 partial round trip through HBM (-8 B
+// written and read per row and slice): iteration i's rows are finished by CTA i mod S (the
+// finishing work — score store, histogram, chunk maxima — rotates over the cluster so no SM does
+// more than its share); the other CTAs send their sums with one st.async per lane into its
+// receive ring, completing on that warp's transaction-count mbarrier. The finishing CTA adds them
+// in slice order in float64 — the chain of the per-slice launches, (((double)p0 + (double)p1) +
+// (double)p2) ..., so scores are bit-identical — and a ring slot is reused only after it released
+// it (a remote arrive on the sender's `empty` barrier).
+constexpr int kBinRing = 4;
+constexpr int kBinWarps = kBinThreads / 32;
+constexpr int kBinMaxS = 8;
+
+__device__ __forceinline__ uint32_t bin_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t bin_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// (default .acquire.cta: the slice sums land by st.async with complete_tx, like TMA writes)
+__device__ __forceinline__ void bin_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+}
+
+template <int RB>
+__global__ void __launch_bounds__(kBinThreads, 1)
+bin_score_cluster(const uint8_t* __restrict__ codes, int64_t n, const double* __restrict__ w, int n_bits,
+                  float* __restrict__ out, uint32_t* __restrict__ ghist, const __grid_constant__ CUtensorMap map,
+                  int use_pf, uint16_t* __restrict__ cmax) {
+  constexpr int S = RB / 128;
+  static_assert(S >= 2 && S <= kBinMaxS, "2..8 slices");
+  extern __shared__ __align__(16) unsigned char tabb[];  // 128 KB table, then the receive ring
+  float* recv = reinterpret_cast<float*>(tabb + 131072);  // [kBinRing][S - 1][kBinWarps][32]
+  __shared__ uint32_t sh[kHistBins];
+  __shared__ __align__(8) uint64_t full[kBinRing][kBinWarps];       // my ring slot (b, warp) landed
+  __shared__ __align__(8) uint64_t empty[S][kBinRing][kBinWarps];   // CTA o read my sums in its slot (b, warp)
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int slice = (int)rank;
+  for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
+    const int l = e & 31, k = (e >> 5) & 3, v = e >> 7;
+    const int bit0 = 8 * (slice * 128 + 4 * l + k);
+    double sum = 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if ((v >> b) & 1) sum = __dadd_rn(sum, bit0 + b < n_bits ? (double)__double2float_rn(w[bit0 + b]) : 0.0);
+    const uint32_t addr = ((uint32_t)(k >> 1) << 16) | ((uint32_t)v << 8) | ((uint32_t)(k & 1) << 7) | ((uint32_t)l << 2);
+    *reinterpret_cast<float*>(tabb + addr) = __double2float_rn(sum);
+  }
+  for (int t = threadIdx.x; t < kBinRing * kBinWarps * (S + 1); t += blockDim.x) {
+    uint64_t* bar = t < kBinRing * kBinWarps ? &full[0][0] + t : &empty[0][0][0] + (t - kBinRing * kBinWarps);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bin_smem_u32(bar)));
+  }
+  if (ghist) hist_zero(sh);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // every CTA's tables and barriers exist before any remote access
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint32_t L = ((uint32_t)lane << 2) | (((uint32_t)lane << 2 | 0x80u) << 8) | (1u << 24);
+  const int64_t cid = blockIdx.x / S, ncl = gridDim.x / S;
+  const uint8_t* base = codes + (int64_t)slice * 128 + 4 * lane;
+  constexpr int R = 32;
+  bool writer;
+  const int slot = row_of_lane<R, 32>(lane, &writer);
+  const int64_t step = ncl * kBinWarps * R;
+  int it = 0;
+  for (int64_t r0 = (cid * kBinWarps + wi) * R; r0 < n; r0 += step, ++it) {
+    if (use_pf && lane == 0) {
+      const int64_t nr = r0 + use_pf * step;
+      if (nr < n)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map), "r"(slice * 128),
+                     "r"((int)nr)
+                     : "memory");
+    }
+    uint32_t wd[R];
+    const uint8_t* rp = base + r0 * RB;
+    if (r0 + R <= n) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) wd[i] = __ldcs(reinterpret_cast<const uint32_t*>(rp + i * RB));
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) wd[i] = r0 + i < n ? __ldcs(reinterpret_cast<const uint32_t*>(rp + i * RB)) : 0u;
+    }
+    float p[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t x = wd[i];
+      float v = *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6604));
+      v = __fadd_rn(v, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6615)));
+      v = __fadd_rn(v, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6724)));
+      v = __fadd_rn(v, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6735)));
+      p[i] = v;
+    }
+    transposed_reduce_f<R, 32>(p, lane);
+    const int o = it % S;  // the CTA that finishes these rows
+    const int j = it / S;  // its j-th finishing iteration
+    const int b = j % kBinRing;
+    const uint32_t ph = (uint32_t)(j / kBinRing) & 1u;
+    if (o != slice) {
+      // the slot's previous contents (o's finishing iteration j - kBinRing) must have been read
+      if (j >= kBinRing) bin_wait(bin_smem_u32(&empty[o][b][wi]), ph ^ 1u);
+      const int q = slice < o ? slice : slice - 1;  // my place among o's senders
+      const uint32_t dst = bin_mapa(bin_smem_u32(recv + (((b * (S - 1) + q) * kBinWarps + wi) << 5) + lane), (uint32_t)o);
+      const uint32_t bar = bin_mapa(bin_smem_u32(&full[b][wi]), (uint32_t)o);
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+                   "r"(__float_as_uint(p[0])), "r"(bar)
+                   : "memory");
+      continue;
+    }
+    const uint32_t fb = bin_smem_u32(&full[b][wi]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"((S - 1) * 32 * 4) : "memory");
+    bin_wait(fb, ph);
+    double total = 0.0;
+    uint32_t dep = 0;
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl) {  // slice order, my own sum in place
+      float v;
+      if (sl == slice) {
+        v = p[0];
+      } else {
+        v = recv[(((b * (S - 1) + (sl < slice ? sl : sl - 1)) * kBinWarps + wi) << 5) + lane];
+        dep |= __float_as_uint(v);
+      }
+      total = sl == 0 ? (double)v : __dadd_rn(total, (double)v);
+    }
+    // release the slot to sender q (lane q): once every lane's read has returned (the arrive's
+    // address depends on the values read, so it cannot be issued earlier; a relaxed arrive: a
+    // .release.cluster one would also wait for this warp's outstanding global stores)
+    dep = __reduce_or_sync(0xffffffffu, dep);
+    asm volatile("and.b32 %0, %0, 0;" : "+r"(dep));  // an opaque zero that waits for the reads
+    if (lane < S - 1) {
+      const uint32_t snd = (uint32_t)(lane < slice ? lane : lane + 1);
+      const uint32_t eb = bin_mapa(bin_smem_u32(&empty[slice][b][wi]) + dep, snd);
+      asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+    }
+    const int64_t row = r0 + slot;
+    const bool active = writer && row < n;
+    const float sc = __double2float_rn(total);
+    if (active) out[row] = sc;
+    if (ghist) hist_add(sh, active, hist_bin(sc));
+    if (cmax) {  // the warp's R consecutive rows are one top-k chunk
+      const uint32_t wm = __reduce_max_sync(0xffffffffu, active ? hist_bin(sc) : 0u);
+      if (lane == 0) cmax[r0 / R] = (uint16_t)wm;
+    }
+  }
+  // no CTA leaves while a peer may still write into its shared memory or arrive on its barriers
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (ghist) hist_flush(sh, ghist);
+}
+
 // Generic path: any n_bits. One warp per row; lane l owns bytes {l + 32*t}, bits in order;
 // float32(w_j) converted on the fly.
 __global__ void __launch_bounds__(256) bin_score_generic(const uint8_t* __restrict__ codes, int64_t n,
@@ -255,6 +414,49 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
         use_pf = 1;  // distance 1..3 iterations measured the same
+    }
+    // The clustered single launch is opt-in (OTF_BIN_CLUSTER=1, read per call): bit-identical,
+    // but measured slower than the per-slice launches on the same boxes (C5a 6.1-6.4 vs 5.7-5.8
+    // ms under sw_power_cap)
+    const char* cl = getenv("OTF_BIN_CLUSTER");
+    if (slices > 1 && cl && cl[0] == '1') {
+      // one launch: clusters of `slices` CTAs, the slice sums meet in the leader's shared memory
+      const int S = slices;
+      const size_t csmem = smem + (size_t)kBinRing * (S - 1) * kBinWarps * 32 * sizeof(float);
+      const void* fn = row_bytes == 256 ? (const void*)bin_score_cluster<256>
+                     : row_bytes == 512 ? (const void*)bin_score_cluster<512> : (const void*)bin_score_cluster<1024>;
+      static bool cconf[64] = {false};
+      if (!cconf[device & 63]) {
+        cudaFuncSetAttribute((const void*)bin_score_cluster<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(smem + (size_t)kBinRing * 1 * kBinWarps * 128));
+        cudaFuncSetAttribute((const void*)bin_score_cluster<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(smem + (size_t)kBinRing * 3 * kBinWarps * 128));
+        cudaFuncSetAttribute((const void*)bin_score_cluster<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(smem + (size_t)kBinRing * 7 * kBinWarps * 128));
+        cudaFuncSetAttribute((const void*)bin_score_cluster<1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cconf[device & 63] = true;
+      }
+      int64_t ncl = sm_count(device) / S;
+      const int64_t cneed = (n + kBinWarps * 32 - 1) / (kBinWarps * 32);
+      if (cneed < ncl) ncl = cneed;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(ncl * S));
+      cfg.blockDim = dim3(kBinThreads);
+      cfg.dynamicSmemBytes = csmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)S;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      void* args[] = {(void*)&codes, (void*)&n, (void*)&w, (void*)&n_bits, (void*)&out, (void*)&hist, (void*)&map,
+                      (void*)&use_pf, (void*)&cmax};
+      OTF_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+      OTF_LAUNCH_CHECK("bin_score_cluster");
+      if (cmax && clog) *clog = 5;
+      return OTF_OK;
     }
     int64_t grid = sm_count(device);  // one 512-thread CTA per SM (128 KB table)
     const int64_t need = (n + (kBinThreads / 32) * 32 - 1) / ((kBinThreads / 32) * 32);

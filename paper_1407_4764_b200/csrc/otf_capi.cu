@@ -327,14 +327,13 @@ int rank_device(otf_repo* r, const double* dw, int64_t k_eff, int64_t* ids, doub
   const uint8_t* codes = static_cast<const uint8_t*>(r->payload);
   int cut_r = 0;
   if (r->kind == OTF_KIND_PQ && pq_cut_plan(r->M, codes, r->n, k_eff, r->device, &cut_r)) {
-    // PQ cut path: LUT kernel, then one cooperative kernel that samples, streams the codes
-    // emitting only the rows that can reach the sampled threshold, and selects among them
+    // PQ cut path: the sample kernel (LUT + sampled threshold), then one cooperative kernel that
+    // streams the codes emitting only the rows that reach the threshold and selects among them
     if ((rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double) * kCutLutReplicas))) return rc;
     if ((rc = topk_cut_alloc(&r->topk))) return rc;
-    if ((rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, dw, static_cast<double*>(r->lut.p), st, kCutLutReplicas)))
-      return rc;
-    return launch_pq_rank_cut(codes, r->n, static_cast<const double*>(r->lut.p), r->K, r->ids, r->id_base, k_eff,
-                              cut_r, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows, r->device, st);
+    return launch_pq_rank_cut(r->cents, r->K, r->Q, dw, static_cast<double*>(r->lut.p), codes, r->n, r->ids,
+                              r->id_base, k_eff, cut_r, &r->topk, static_cast<double*>(r->scores.p), ids, scores, rows,
+                              r->device, st);
   }
   if (r->kind == OTF_KIND_PQ && pq_bins_path(r->M, codes)) {
     // PQ: the scan writes 2-byte bins, the top-k recomputes the candidates' exact scores
@@ -589,8 +588,6 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* 
   if (!rc && cut) rc = topk_cut_alloc(&r->topk);
   if (!rc && cut) rc = topk_ws_alloc(&r->topk, k_eff);
   if (!rc && cut) rc = r->outbuf.ensure((size_t)(k_eff > 0 ? k_eff : 1) * 24);
-  if (!rc && cut && !dcut)
-    rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st, kCutLutReplicas);
   if (!rc && bins) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(uint16_t));
   if (!rc && bins) rc = r->lut.ensure((size_t)r->M * r->K * sizeof(double));
   if (!rc && bins) rc = launch_pq_lut(r->cents, r->M, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), st);
@@ -606,11 +603,11 @@ int otf_repo_time_rank_scan(otf_repo* r, const double* w_dev, int64_t k, float* 
                                k_eff, dpl, &r->topk, static_cast<float*>(r->scores.p), d_ids,
                                reinterpret_cast<double*>(d_ids + k_eff), d_ids + 2 * k_eff, st);
   } else if (cut) {
-    // the fused kernel is the rank path's scoring kernel (scan + selection in one launch)
+    // the PQ cut path's two kernels (sample + LUT, scan + selection) are the rank path's scan
     int64_t* d_ids = static_cast<int64_t*>(r->outbuf.p);
-    rc = launch_pq_rank_cut(codes, r->n, static_cast<const double*>(r->lut.p), r->K, r->ids, r->id_base, k_eff, cut_r,
-                            &r->topk, static_cast<double*>(r->scores.p), d_ids, reinterpret_cast<double*>(d_ids + k_eff),
-                            d_ids + 2 * k_eff, r->device, st);
+    rc = launch_pq_rank_cut(r->cents, r->K, r->Q, w_dev, static_cast<double*>(r->lut.p), codes, r->n, r->ids,
+                            r->id_base, k_eff, cut_r, &r->topk, static_cast<double*>(r->scores.p), d_ids,
+                            reinterpret_cast<double*>(d_ids + k_eff), d_ids + 2 * k_eff, r->device, st);
   } else if (bins)
     rc = launch_pq_scan_bins(codes, r->n, static_cast<const double*>(r->lut.p), r->K,
                              static_cast<uint16_t*>(r->bins.p), r->topk.hist, r->device, st, r->topk.cmax, &clog);

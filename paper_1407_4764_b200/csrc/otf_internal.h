@@ -111,15 +111,16 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
 int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base,
                          int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores, int device,
                          cudaStream_t st);
-// PQ cut path (M == 16, large n): one cooperative kernel after the LUT kernel — samples the
-// score distribution, streams the codes emitting only the rows that can reach the sampled
-// threshold, and selects the exact top-k among them (or falls back to an exact select over every
-// row); see otf_pq.cu pq_rank_cut_kernel. pq_cut_plan returns r (the sample rank of the
-// threshold) or false when the path does not apply (small n or large k).
+// PQ cut path (M == 16, large n): a sample kernel (the float64 LUT and its replicas in `lut`,
+// a sampled threshold), then one cooperative kernel that streams the codes emitting only the
+// rows that reach the threshold and selects the exact top-k among them (or falls back to an
+// exact select over every row); see otf_pq.cu pq_rank_cut_kernel. pq_cut_plan returns r (the
+// sample rank of the threshold) or false when the path does not apply (small n or large k).
 bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int device, int* r);
-int launch_pq_rank_cut(const uint8_t* codes, int64_t n, const double* lut, int K, const int64_t* ids,
-                       int64_t id_base, int64_t k_eff, int r, TopkWs* ws, double* scratch, int64_t* out_ids,
-                       double* out_scores, int64_t* out_rows, int device, cudaStream_t st);
+int launch_pq_rank_cut(const float* cents, int K, int Q, const double* w, double* lut, const uint8_t* codes,
+                       int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, int r, TopkWs* ws,
+                       double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows, int device,
+                       cudaStream_t st);
 int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,
                         int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, TopkWs* ws,
                         double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows,

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
                                                                      uint16_t* __restrict__ bins_out,
                                                                      uint32_t* __restrict__ ghist,
                                                                      uint16_t* __restrict__ cmax) {
-  extern __shared__ __align__(256) unsigned char sm[];  // [256 lines x 256 B][hist][m maxima]
+  extern __shared__ __align__(1024) unsigned char sm[];  // [256 lines x 256 B][hist][m maxima]
   uint32_t* sh = reinterpret_cast<uint32_t*>(sm + 65536);
   uint32_t* smax = sh + kPqHistBins;
   if (threadIdx.x < 16) smax[threadIdx.x] = 0u;
@@ -579,25 +579,27 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
 
 // ---- M == 16 cut path: one cooperative kernel (sampled threshold, candidate emission, select) ---
 // The rank path needs the k best rows, not every row's score. pq_rank_cut_kernel (one CTA per SM,
-// cooperative) streams the codes of its contiguous range of 2048-row chunks through shared
+// cooperative, launched programmatically after the LUT kernel) streams the codes through shared
 // memory (1-D bulk copies, see below) and
-//   1. scores its FIRST chunk (a sample spread over the whole repository: one chunk per CTA) and
-//      publishes the sample's two largest screening scores; one grid barrier; every CTA takes
-//      T = the r-th largest of those 2 G values (r ~ 2 k_eff x sample / n, so ~2 k_eff rows
-//      are expected at or above T) and rounds it down to the lower edge of its 13-bit bin;
-//   2. keeps only the rows whose float32 screening score s32 can reach that edge (s32 >= T - 2
-//      eps, |s32 - s64| <= eps as in pq_scan16_f32bins): their exact float64 score (numpy's
-//      order, from the float64 LUT in shared memory) and row go to a candidate list and their
-//      exact bin to a histogram (global atomics: candidates are ~0.02% of the rows); nothing is
-//      written for the other rows (no per-row bins, no per-row histogram updates);
-//   3. one more grid barrier; every CTA finds the bin b0 of the k-th best candidate. All rows
-//      whose exact score lies in T's bin or above are candidates, so when b0 >= that bin the
-//      global top-k is among them: each CTA copies the candidates of bins >= b0 into its shared
-//      memory in list order (the same array in every CTA) and ranks its share by counting
-//      (candidate i on CTA i mod G), writing each to its output slot. Otherwise (T too high:
-//      fewer than k rows reached it, or more than kCutCap candidates: heavy ties, w = 0, a
-//      non-finite LUT) the kernel computes every row's exact score and runs the exact radix
-//      select (otf_topk_dev.cuh) — slower, same result.
+//   1. scores the first half of its first chunk (a sample spread over the whole repository: 2048
+//      rows per CTA) in float32 and publishes the sample's two largest screening keys; a SPLIT
+//      grid barrier: while the other CTAs finish their sample, each CTA scores the next three
+//      batches of its ring (held: their screening scores stay in registers, their codes in the
+//      stages); then every CTA takes T = the r-th largest of the 2 G published keys at 16-bit key
+//      resolution (r ~ (2 k_eff + 128) x sample / n, so ~2 k_eff + 128 rows are expected at or
+//      above T), rounded down to that prefix's lower edge;
+//   2. emits every row whose float32 screening score s32 can reach T (s32 >= T - eps, |s32 -
+//      s64| <= eps as in pq_scan16_f32bins) AND whose exact float64 score (numpy's order, from
+//      the float64 LUT in shared memory) is >= T: (exact key, ~id), the row and the key's top 32
+//      bits go to a candidate list (warp-aggregated atomics; ~0.02% of the rows); nothing is
+//      written for the other rows (no per-row bins, histogram or score writes);
+//   3. one more grid barrier; every row with exact score >= T is a candidate, so when at least
+//      k_eff and at most kRcCand rows reached T the global top-k is among them: every CTA copies
+//      the candidates' 32-bit key prefixes into shared memory and ranks its share by counting
+//      (candidate i on CTA i mod G; full keys, ids and rows read only for prefix ties), writing
+//      each straight to its output slot. Otherwise (T too high: fewer than k rows reached it; or
+//      too many candidates: heavy ties, w = 0; or a non-finite LUT) the kernel computes every
+//      row's exact score and runs the exact radix select (otf_topk_dev.cuh) — slower, same result.
 // Bit-exact with the reference either way (pq.py:248-276 scores, ranker.py:97-143 order).
 #ifdef OTF_CUT_TRACE  // diagnostic build (tools/gpu_cut_trace.sh): per-CTA globaltimer stamps
 #define CUT_STAMP(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[i]))
@@ -609,28 +611,21 @@ __device__ __forceinline__ float key_to_f32(uint32_t k) {
   return __uint_as_float((k >> 31) ? (k ^ 0x80000000u) : ~k);
 }
 
-// Rare: the lanes with emit bits append (exact float64 key, ~id) and the row of those rows
-// (warp-aggregated slot reservation). The record is self-contained, so the selection reads each
-// candidate once.
+// Rare: the lanes with screening bits compute their rows' exact float64 score (numpy's pairwise
+// order from the float64 entries of the LUT lines); rows whose exact key reaches T append
+// (exact key, ~id), the row and the key's top 32 bits (warp-aggregated slot reservation).
 template <int ROWS>
 __device__ __noinline__ void cut_emit(const unsigned char* sm, uint4 u0, uint4 u1, uint4 u2, uint4 u3, uint32_t emit,
                                       int64_t row0, const int64_t* ids, int64_t id_base,
-                                      unsigned long long* cut_count, unsigned long long* cut_ge, uint64_t tkey64,
-                                      ulonglong2* cut_rec, int64_t* cut_row, int64_t cut_cap) {
+                                      unsigned long long* cut_count, uint64_t tkey64, ulonglong2* cut_rec,
+                                      int64_t* cut_row, uint32_t* key32, int64_t cut_cap, int64_t key32_cap) {
   static_assert(ROWS == 4, "four rows per lane");
   const int lane = threadIdx.x & 31;
   const uint4 uu[4] = {u0, u1, u2, u3};
-  uint32_t ge = 0;
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) {
-    const bool take = (emit >> i) & 1u;
-    const unsigned bal = __ballot_sync(0xffffffffu, take);
-    if (bal == 0u) continue;
-    unsigned long long slot0 = 0;
-    if (lane == 0) slot0 = atomicAdd(cut_count, (unsigned long long)__popc(bal));
-    const int64_t slot = (int64_t)__shfl_sync(0xffffffffu, slot0, 0) + __popc(bal & ((1u << lane) - 1u));
-    // past the capacity only the count matters (the selection falls back)
-    if (take && slot < cut_cap) {
+    uint64_t key = 0;
+    if ((emit >> i) & 1u) {
       const uint32_t xw[4] = {uu[i].x, uu[i].y, uu[i].z, uu[i].w};
       double a[16];
 #pragma unroll
@@ -641,17 +636,22 @@ __device__ __noinline__ void cut_emit(const unsigned char* sm, uint4 u0, uint4 u
       for (int j = 0; j < 8; ++j) rr[j] = __dadd_rn(a[j], a[j + 8]);
       const double ex = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
                                   __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+      key = score_key(ex);
+    }
+    const bool take = ((emit >> i) & 1u) && key >= tkey64;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (bal == 0u) continue;
+    unsigned long long slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(cut_count, (unsigned long long)__popc(bal));
+    const int64_t slot = (int64_t)__shfl_sync(0xffffffffu, slot0, 0) + __popc(bal & ((1u << lane) - 1u));
+    // past the capacity only the count matters (the selection falls back)
+    if (take && slot < cut_cap) {
       const int64_t row = row0 + 32 * i;
-      const uint64_t key = score_key(ex);
       cut_rec[slot] = make_ulonglong2(key, inv_id(id_of(ids, id_base, row)));
       cut_row[slot] = row;
-      ge |= (key >= tkey64) << i;
+      if (slot < key32_cap) key32[slot] = (uint32_t)(key >> 32);
     }
   }
-  // candidates at or above T (the exact test the selection relies on), one atomic per warp
-  const unsigned n_ge = (unsigned)__popc(ge);
-  const unsigned tot = __reduce_add_sync(0xffffffffu, n_ge);
-  if (lane == 0 && tot) atomicAdd(cut_ge, (unsigned long long)tot);
 }
 
 // The codes stream through shared memory: 4096-row chunks (64 KB) land by 1-D bulk copies
@@ -733,11 +733,8 @@ __device__ __forceinline__ void cut_scores(const unsigned char* sm, const uint4 
 }
 
 constexpr size_t kRcSmem = 256 * 256 + (size_t)kCutStages * kCutChunkBytes;  // 192 KB
-constexpr int kRcCand = 4096;  // candidates the selection ranks in shared memory
-constexpr int kCutSelCtas = 1024;  // CTAs that select + rank (all: the ranking's shared traffic is ~C^2 / #CTAs)
-// selection layout in the (reused) dynamic shared memory: (key, inv) pairs, rows, 8192-bin histogram
-constexpr size_t kRcPairs = 0, kRcRows = (size_t)kRcCand * 16;
-static_assert(kRcRows + (size_t)kRcCand * 8 <= kRcSmem, "selection reuses the scan's shared memory");
+constexpr int kRcCand = 8192;  // candidates the selection ranks in shared memory (32-bit key prefixes)
+static_assert((size_t)kRcCand * 4 <= kRcSmem, "selection reuses the scan's shared memory");
 
 // max of four floats (emission test of a batch: one compare instead of four)
 __device__ __forceinline__ float max4(const float (&v)[4]) { return fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])); }
@@ -752,19 +749,17 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* stage = sm + 65536;
   __shared__ __align__(8) uint64_t full[kCutStages];
-  __shared__ __align__(8) uint64_t sbar;  // the sample: the first half of chunk 0, requested first
+  __shared__ __align__(8) uint64_t sbar;  // the sample: the first half of chunk c0, requested first
   __shared__ __align__(8) uint64_t lbar;  // the LUT replica (into the second half of stage 0)
   __shared__ unsigned done[kCutStages];
   __shared__ int64_t stage_chunk[kCutStages];  // chunk held by each stage (-1: none left)
   __shared__ uint32_t smx[16];
   __shared__ uint32_t s_top[2 * (kCutScanThreads / 32)];
-  __shared__ __align__(16) uint32_t s_all[kCutScanThreads];
   __shared__ uint32_t s_tkey;
   __shared__ uint32_t h[256];
   __shared__ int s_b;
   __shared__ int64_t s_above;
-  __shared__ unsigned s_wpre[33];
-  __shared__ unsigned s_last;
+  __shared__ unsigned s_last, s_gen;
 #ifdef OTF_CUT_TRACE
   unsigned long long ts[7] = {0, 0, 0, 0, 0, 0, 0};
   CUT_STAMP(0);
@@ -777,7 +772,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   // stream faster take more chunks and all finish together
   const int64_t nchunks = (n + kCutChunkRows - 1) / kCutChunkRows;  // >= 4 G (pq_cut_plan)
   const int64_t c0 = (int64_t)vb * nchunks / G;
-  const int64_t rb = c0 * kCutChunkRows, re = n;  // rows of chunk c: [c * kCutChunkRows, min(+, n))
+  const int64_t rb = c0 * kCutChunkRows, re = n;
   auto next_chunk = [&]() -> int64_t {  // the next dynamically assigned chunk, or -1
     for (;;) {
       const int64_t c = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(ws.cut_word + 8), 1ull);
@@ -795,7 +790,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&sbar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&lbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the codes do not depend on the LUT kernel: the sample (batch 0 of chunk 0) and chunk 1
+    // the codes do not depend on the LUT kernel: the sample (batch 0 of chunk c0) and chunk 1
     // stream in while it finishes
     cut_issue(codes, re, rb, stage, &sbar, kCutBatchRows);
     stage_chunk[0] = c0;
@@ -841,11 +836,10 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
     if (lane < 16) atomicMax(&smx[m], mx);
   }
-  __syncthreads();  // every read of the raw LUT is done: chunk 0's second half may land there
+  __syncthreads();  // every read of the raw LUT is done: chunk c0's second half may land there
   if (threadIdx.x == 0)
     cut_issue(codes, re, rb + kCutBatchRows, stage + kCutBatchRows * 16, &full[0], kCutChunkRows - kCutBatchRows);
-  // (rows of c0 past n: the second half may be empty for a last partial chunk; pq_cut_plan keeps
-  // c0 + 1 <= nchunks - 1 so chunk c0 is full)
+  // (pq_cut_plan keeps c0 + 1 <= nchunks - 1, so chunk c0 is full)
   float eps;
   bool screen;
   {
@@ -867,18 +861,18 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
 #pragma unroll
   for (int q = 0; q < 4; ++q) sel[q] = 0x7604u | (uint32_t)(q & 1) | ((((uint32_t)q ^ s) & 3u) << 4);
   unsigned long long* cut_count = reinterpret_cast<unsigned long long*>(ws.cut_word);
-  unsigned long long* cut_ge = reinterpret_cast<unsigned long long*>(ws.cut_word + 4);
   ulonglong2* cut_rec = reinterpret_cast<ulonglong2*>(ws.cut_key);
+  uint32_t* key32 = reinterpret_cast<uint32_t*>(ws.key);  // prefixes of the first kRcCand candidates
+  const int boff = wid * (32 * ROWS) + lane;  // this lane's first row inside a batch
 
-  // ---- 1. the sample: batch 0 of this CTA's first chunk ------------------------------------------
-  // batch bt of warp w: rows [bt * kCutBatchRows + 128 w, + 128) of the chunk
+  // ---- 1. the sample: batch 0 of chunk c0 ----------------------------------------------------------
   uint4 u0[ROWS];
   float s0[ROWS];
-  const int64_t row00 = rb + wid * (32 * ROWS) + lane;
+  const int64_t row00 = rb + boff;
   {
     uint32_t ka = 0u, kb = 0u;  // this lane's two largest sample keys (0: below every key)
     cut_wait(&sbar, 0u);
-    const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + wid * (32 * ROWS) + lane;
+    const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + boff;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) u0[i] = row00 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
     cut_scores<ROWS>(sm, u0, kw, sel, s, s0);
@@ -899,7 +893,35 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     }
   }
   CUT_STAMP(1);
-  grid_barrier(ws.bar, G);
+  // split grid barrier: while the other CTAs finish their sample, score the three batches already
+  // in the ring (chunk c0's second half, the whole chunk in stage 1) and hold their scores
+  const unsigned gen = grid_arrive(ws.bar, G, &s_gen);
+  float hs[3][ROWS];
+  const int64_t c1 = stage_chunk[1];
+  {
+    cut_wait(&full[0], 0u);
+    const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + kCutBatchRows + boff;
+    uint4 u[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) u[i] = rows4[32 * i];
+    cut_scores<ROWS>(sm, u, kw, sel, s, hs[0]);
+    cut_wait(&full[1], 0u);
+#pragma unroll
+    for (int bt = 0; bt < 2; ++bt) {
+      if (c1 >= 0) {
+        const int64_t r0 = c1 * kCutChunkRows + bt * kCutBatchRows + boff;
+        const uint4* q4 = reinterpret_cast<const uint4*>(stage + kCutChunkBytes) + bt * kCutBatchRows + boff;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) u[i] = r0 + 32 * i < re ? q4[32 * i] : make_uint4(0, 0, 0, 0);
+        cut_scores<ROWS>(sm, u, kw, sel, s, hs[1 + bt]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) hs[1 + bt][i] = -INFINITY;
+      }
+    }
+  }
+  grid_wait(ws.bar, gen);
+  CUT_STAMP(2);
   // T = the r-th largest of the 2 G sample maxima at 16-bit key resolution (two 8-bit radix
   // passes in shared memory), rounded down to that key's lower edge
   {
@@ -913,7 +935,6 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       if (threadIdx.x < 256) h[threadIdx.x] = 0u;
       __syncthreads();
       if (real && (pass == 0 || (v >> 24) == prefix)) atomicAdd(&h[(v >> shift) & 255u], 1u);
-      __syncthreads();
       const int have = __syncthreads_count(real && (pass == 0 || (v >> 24) == prefix));
       if (have < need) break;  // fewer than r sampled values (uniform)
       pick_bin256(h, need, &s_b, &s_above);
@@ -927,52 +948,65 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   }
   const uint32_t tkey = s_tkey;
   const float T = key_to_f32(tkey);
-  // every row whose exact score x >= T has s32 >= x - eps >= T - eps: it is emitted
+  // every row whose exact score x >= T has s32 >= x - eps >= T - eps: it is screened in
   const float t_emit = __fsub_rd(T, eps);
   const bool usable = screen && tkey != 0u && !isnan(t_emit) && !isinf(T);
   const uint64_t tkey64 = score_key((double)T);
-  CUT_STAMP(2);
+  CUT_STAMP(3);
 
-  // ---- 2. emission: the held sample rows, then the rest of the range ------------------------------
-  if (usable && __any_sync(0xffffffffu, max4(s0) >= t_emit)) {
+  // ---- 2. emission: the sample rows, the held batches, then the rest of the codes ------------------
+  auto emit_batch = [&](const uint4 (&u)[ROWS], const float (&sc)[ROWS], int64_t row0) {
     uint32_t emit = 0;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i)
-      if (s0[i] >= t_emit && row00 + 32 * i < re) emit |= 1u << i;
-    cut_emit<ROWS>(sm, u0[0], u0[1], u0[2], u0[3], emit, row00, ids, id_base, cut_count, cut_ge, tkey64, cut_rec,
-                   ws.cut_row, ws.cut_cap);
-  }
-  for (int64_t j = 0;; ++j) {
-    const int st = (int)(j % kCutStages);
-    cut_wait(&full[st], (uint32_t)((j / kCutStages) & 1));  // (j == 0: the second half of chunk c0)
-    const int64_t c = stage_chunk[st];
-    if (c < 0) break;
-    const int64_t cr0 = c * kCutChunkRows;
-    const bool full_chunk = cr0 + kCutChunkRows <= re;
+      if (sc[i] >= t_emit && row0 + 32 * i < re) emit |= 1u << i;
+    cut_emit<ROWS>(sm, u[0], u[1], u[2], u[3], emit, row0, ids, id_base, cut_count, tkey64, cut_rec, ws.cut_row,
+                   key32, ws.cut_cap, kRcCand);
+  };
+  if (usable) {
+    if (__any_sync(0xffffffffu, max4(s0) >= t_emit)) emit_batch(u0, s0, row00);
 #pragma unroll 1
-    for (int bt = (j == 0 ? 1 : 0); bt < kCutBatches; ++bt) {
-      const int off = bt * kCutBatchRows + wid * (32 * ROWS) + lane;
-      const uint4* rows4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + off;
-      const int64_t row0 = cr0 + off;
+    for (int hb = 0; hb < 3; ++hb) {  // (the held batches' codes are still in their stages)
+      if (!__any_sync(0xffffffffu, max4(hs[hb]) >= t_emit)) continue;
+      const int st = hb == 0 ? 0 : 1;
+      const int bt = hb == 0 ? 1 : hb - 1;
+      const int64_t r0 = (hb == 0 ? c0 : c1) * kCutChunkRows + bt * kCutBatchRows + boff;
+      const uint4* q4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + bt * kCutBatchRows + boff;
       uint4 u[ROWS];
-      float sc[ROWS];
-      if (full_chunk) {
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) u[i] = rows4[32 * i];
-      } else {
+      for (int i = 0; i < ROWS; ++i) u[i] = r0 + 32 * i < re ? q4[32 * i] : make_uint4(0, 0, 0, 0);
+      emit_batch(u, hs[hb], r0);
+    }
+  }
+  // both stages are consumed: the last warp done with each refills it
+  for (int j = 0;; ++j) {
+    const int st = j % kCutStages;
+    if (j >= kCutStages) {
+      cut_wait(&full[st], (uint32_t)((j / kCutStages) & 1));
+      const int64_t c = stage_chunk[st];
+      if (c < 0) break;
+      const int64_t cr0 = c * kCutChunkRows;
+      const bool full_chunk = cr0 + kCutChunkRows <= re;
+#pragma unroll 1
+      for (int bt = 0; bt < kCutBatches; ++bt) {
+        const int off = bt * kCutBatchRows + boff;
+        const uint4* rows4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + off;
+        const int64_t row0 = cr0 + off;
+        uint4 u[ROWS];
+        float sc[ROWS];
+        if (full_chunk) {
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) u[i] = row0 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
+          for (int i = 0; i < ROWS; ++i) u[i] = rows4[32 * i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < ROWS; ++i) u[i] = row0 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
+        }
+        if (!usable) continue;
+        cut_scores<ROWS>(sm, u, kw, sel, s, sc);
+        if (__any_sync(0xffffffffu, max4(sc) >= t_emit)) emit_batch(u, sc, row0);
       }
-      if (!usable) continue;
-      cut_scores<ROWS>(sm, u, kw, sel, s, sc);
-      if (__any_sync(0xffffffffu, max4(sc) >= t_emit)) {
-        uint32_t emit = 0;
-#pragma unroll
-        for (int i = 0; i < ROWS; ++i)
-          if (sc[i] >= t_emit && row0 + 32 * i < re) emit |= 1u << i;
-        cut_emit<ROWS>(sm, u[0], u[1], u[2], u[3], emit, row0, ids, id_base, cut_count, cut_ge, tkey64, cut_rec,
-                       ws.cut_row, ws.cut_cap);
-      }
+    } else if (stage_chunk[st] < 0) {
+      break;
     }
     __syncwarp();  // this warp's reads of the stage are complete (consumed above)
     if (lane == 0 && atomicAdd(&done[st], 1u) == (unsigned)(nw - 1)) {
@@ -983,100 +1017,61 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
     }
   }
-  CUT_STAMP(3);
-  grid_barrier(ws.bar, G);  // every candidate record is in place
   CUT_STAMP(4);
+  grid_barrier(ws.bar, G);  // every candidate record is in place
+  CUT_STAMP(5);
 
   // ---- 3. selection ----------------------------------------------------------------------------
-  // Every row with exact score >= T is a candidate, so when at least k_eff candidates are >= T
-  // the global top-k is among those: the first kCutSelCtas CTAs copy them (list order, the same
-  // array in every CTA) into shared memory and rank them by counting. All CTAs decide the branch
-  // from the same two counters.
-  const unsigned long long c_all = __ldcg(cut_count), c_ge = __ldcg(cut_ge);
-  constexpr int kHeld = 8;  // records per thread: 4096 candidates
-  const bool ok = usable && c_all <= (unsigned long long)(kHeld * kCutScanThreads) && c_ge >= (unsigned long long)k_eff;
-  const unsigned gsel = min(G, (unsigned)kCutSelCtas);
+  const unsigned long long c_all = __ldcg(cut_count);
+  const bool ok = usable && c_all >= (unsigned long long)k_eff && c_all <= (unsigned long long)kRcCand;
   // the last CTA done with the shared counters clears them for the next query
-  auto leave = [&]() {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
-      if (s_last) { ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[4] = 0u; ws.cut_word[5] = 0u;
-                    ws.cut_word[8] = 0u; ws.cut_word[9] = 0u; ws.cut_word[6] = 0u; }
-    }
-  };
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
+    if (s_last) { ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[8] = 0u; ws.cut_word[9] = 0u; ws.cut_word[6] = 0u; }
+  }
   if (ok) {
-    if (vb >= gsel) { leave(); return; }
-    ulonglong2* pairs = reinterpret_cast<ulonglong2*>(sm + kRcPairs);
-    int64_t* prow = reinterpret_cast<int64_t*>(sm + kRcRows);
-    const int m = (int)c_all;
-    const int e0 = (int)threadIdx.x * kHeld;
-    const int mine = max(0, min(kHeld, m - e0));
-    ulonglong2 rec[kHeld];
-    int64_t rws[kHeld];
-#pragma unroll
-    for (int q = 0; q < kHeld; ++q) {
-      rec[q] = q < mine ? __ldcg(cut_rec + e0 + q) : make_ulonglong2(0ull, 0ull);
-      rws[q] = q < mine ? __ldcg(ws.cut_row + e0 + q) : 0;
-    }
-    int kept = 0;
-#pragma unroll
-    for (int q = 0; q < kHeld; ++q) kept += (q < mine && rec[q].x >= tkey64);
-    unsigned incl = (unsigned)kept;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_wpre[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      const unsigned y = lane < nw ? s_wpre[lane] : 0u;
-      unsigned x = y;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned z = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += z;
-      }
-      s_wpre[lane] = x - y;
-    }
-    __syncthreads();
-    int pos = (int)(s_wpre[wid] + incl - (unsigned)kept);
-#pragma unroll
-    for (int q = 0; q < kHeld; ++q)
-      if (q < mine && rec[q].x >= tkey64) {
-        pairs[pos] = rec[q];
-        prow[pos] = rws[q];
-        ++pos;
-      }
-    CUT_STAMP(5);
-    leave();
-    __syncthreads();
-    const int C = (int)c_ge;
-    // rank candidates i == vb (mod gsel): one warp per candidate counts who beats it
-    for (int q = (int)vb + wid * (int)gsel; q < C; q += nw * (int)gsel) {
-      const ulonglong2 ci = pairs[q];
-      int cnt = 0;
+    uint32_t* sk = reinterpret_cast<uint32_t*>(sm);
+    const int C = (int)c_all;
 #pragma unroll 4
+    for (int t = threadIdx.x; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
+    __syncthreads();
+    // rank candidates i == vb (mod G): one warp per candidate counts who beats it
+    for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
+      const uint32_t ki = sk[q];
+      int cnt = 0;
+      unsigned tie = 0;
+#pragma unroll 8
       for (int jj = lane; jj < C; jj += 32) {
-        const ulonglong2 cj = pairs[jj];
-        cnt += cand_greater(cj.x, cj.y, ci.x, ci.y);
+        const uint32_t kj = sk[jj];
+        cnt += kj > ki;
+        tie |= kj == ki && jj != q;
+      }
+      const ulonglong2 ci = __ldcg(cut_rec + q);
+      if (__any_sync(0xffffffffu, tie)) {  // equal prefixes: the full key, then ~id, then the row
+        const int64_t ri = __ldcg(ws.cut_row + q);
+        for (int jj = lane; jj < C; jj += 32) {
+          if (sk[jj] != ki || jj == q) continue;
+          const ulonglong2 cj = __ldcg(cut_rec + jj);
+          cnt += cand_greater(cj.x, cj.y, ci.x, ci.y) ||
+                 (cj.x == ci.x && cj.y == ci.y && __ldcg(ws.cut_row + jj) < ri);
+        }
       }
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       if (lane == 0 && cnt < k_eff) {
         out_ids[cnt] = id_of_inv(ci.y);
         out_scores[cnt] = key_to_f64(ci.x);
-        if (out_rows) out_rows[cnt] = prow[q];
+        if (out_rows) out_rows[cnt] = __ldcg(ws.cut_row + q);
       }
     }
 #ifdef OTF_CUT_TRACE
     CUT_STAMP(6);
     if (threadIdx.x == 0)
-      printf("cutT cta %d C_all %llu C %d sample %.2f threshold %.2f scan %.2f barrier %.2f select %.2f rank %.2f total %.2f\n",
-             (int)vb, c_all, C, (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3,
-             (ts[4] - ts[3]) * 1e-3, (ts[5] - ts[4]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[6] - ts[0]) * 1e-3);
+      printf("cutT cta %d C %d sample %.2f held %.2f threshold %.2f scan %.2f barrier %.2f select %.2f total %.2f\n",
+             (int)vb, C, (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3,
+             (ts[5] - ts[4]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[6] - ts[0]) * 1e-3);
 #endif
     return;
   }
@@ -1087,11 +1082,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   const int64_t nthreads = (int64_t)G * blockDim.x;
   for (int64_t i = (int64_t)vb * blockDim.x + threadIdx.x; i < n; i += nthreads) scratch[i] = src.exact(i, 0u);
   grid_barrier(ws.bar, G);
-  if (vb == 0 && threadIdx.x == 0) {
-    ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[4] = 0u; ws.cut_word[5] = 0u;
-    ws.cut_word[8] = 0u; ws.cut_word[9] = 0u;
-    ws.cut_word[3] += 1u;  // fallbacks taken (diagnostics: otf_repo_cut_fallbacks)
-  }
+  if (vb == 0 && threadIdx.x == 0) ws.cut_word[3] += 1u;  // fallbacks taken (diagnostics: otf_repo_cut_fallbacks)
   radix_select_emit(static_cast<const double*>(scratch), src, n, ids, id_base, k_eff, ws, k_eff >= n, sm, out_ids,
                     out_scores, out_rows, h, &s_b, &s_above, vb, G);
 }
@@ -1105,17 +1096,22 @@ bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int devi
   const int64_t S = (int64_t)g * kCutBatchRows;            // batch 0 of every CTA's first chunk
   // ~2 k_eff + 128 rows are expected at or above the r-th largest of the S sampled scores (the
   // r-th order statistic of the sample: relative spread ~1/sqrt(r), so fewer than k_eff rows or
-  // more than the 4096 candidate slots of the selection are both many sigmas away); the CTAs
+  // more than the kRcCand candidate slots of the selection are both many sigmas away); the CTAs
   // publish their top two, so r <= g / 2 keeps the estimate close to the true r-th sample
-  const int64_t rr = ((2 * k_eff + 128) * S + n - 1) / n;
+  const int64_t want = 2 * k_eff + 128;
+  if (2 * want > kRcCand) return false;
+  const int64_t rr = (want * S + n - 1) / n;
   if (rr > g / 2) return false;
   *r = (int)std::max<int64_t>(rr, 1);
   return true;
 }
 
-int launch_pq_rank_cut(const uint8_t* codes, int64_t n, const double* lut, int K, const int64_t* ids,
-                       int64_t id_base, int64_t k_eff, int r, TopkWs* ws, double* scratch, int64_t* out_ids,
-                       double* out_scores, int64_t* out_rows, int device, cudaStream_t st) {
+int launch_pq_rank_cut(const float* cents, int K, int Q, const double* w, double* lut, const uint8_t* codes,
+                       int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff, int r, TopkWs* ws,
+                       double* scratch, int64_t* out_ids, double* out_scores, int64_t* out_rows, int device,
+                       cudaStream_t st) {
+  int rc = launch_pq_lut(cents, 16, K, Q, w, lut, st, kCutLutReplicas);
+  if (rc) return rc;
   auto fn = pq_rank_cut_kernel;
   static bool configured[64] = {false};
   if (!configured[device & 63]) {
@@ -1136,8 +1132,8 @@ int launch_pq_rank_cut(const uint8_t* codes, int64_t n, const double* lut, int K
   cfg.attrs = attr;
   static const bool no_pdl = getenv("OTF_PQ_NO_PDL") != nullptr;
   cfg.numAttrs = no_pdl ? 1 : 2;
-  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, codes, n, lut, K, ids, id_base, k_eff, r, *ws, scratch, out_ids, out_scores,
-                              out_rows));
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, codes, n, static_cast<const double*>(lut), K, ids, id_base, k_eff, r, *ws,
+                              scratch, out_ids, out_scores, out_rows));
   OTF_LAUNCH_CHECK("pq_rank_cut_kernel");
   return OTF_OK;
 }

@@ -71,7 +71,7 @@ def test_cut_fallback_all_tied(otf, data):
 
 
 def test_cut_fallback_threshold_too_high(otf, data):
-    """Adversarial layout: one sampled row per CTA (the first of its range) holds the best codes,
+    """Adversarial layout: one sampled row per sample CTA (the first of its chunk) holds the best codes,
     so the sampled threshold sits in the top bin, which ~150 rows reach: fewer than k -> the
     selection must fall back and still return the exact top-k."""
     cents, codes0 = data
@@ -80,7 +80,8 @@ def test_cut_fallback_threshold_too_high(otf, data):
     lut = O.build_score_lut(w, cents)
     best = np.argmax(lut, axis=1).astype(np.uint8)
     g = 148
-    sampled = np.arange(g) * N // g  # the first row of every CTA's range (part of its sample)
+    nchunks = -(-N // 2048)
+    sampled = np.arange(g) * nchunks // g * 2048  # the first row of every sample CTA's chunk
     codes[sampled] = best
     repo = otf.Repository.quantized(otf.PQCodebook(cents), codes)
     f0 = fallbacks(otf, repo)
