@@ -43,6 +43,9 @@ extern "C" {
 #define OTF_ERR_EMPTY 5        /* EmptyStoreError        errors.py:22 */
 #define OTF_ERR_CUDA 6         /* RetrievalError         errors.py:10 (CUDA failure) */
 #define OTF_ERR_NCCL 7         /* RetrievalError         errors.py:10 (collective)   */
+#define OTF_ERR_FORMAT 8       /* FormatError            errors.py:14 (magic / version) */
+#define OTF_ERR_DEGENERATE 9   /* DegenerateInputError   errors.py:26 (zero-norm row) */
+#define OTF_ERR_IO 10          /* OSError (open / read of a repository file)           */
 
 #define OTF_MEM_HOST 0
 #define OTF_MEM_DEVICE 1
@@ -93,6 +96,29 @@ int otf_repo_create_binary(int device, const uint8_t* codes, int64_t n, int32_t 
 int otf_repo_subset(const otf_repo* src, const int64_t* rows, int64_t n_keep, otf_repo** out);
 
 int otf_repo_destroy(otf_repo* repo);
+
+/* ---- repository files straight into HBM (§8 f3) --------------------------------------- *
+ * The reference loads a file into a host numpy array and then builds the Repository; these read
+ * the file in chunks into pinned staging buffers and copy each chunk to the repository's HBM
+ * while the next is read (no host-side array of the payload). Header checks and errors follow
+ * formats.py: bad magic / version -> OTF_ERR_FORMAT, short file -> OTF_ERR_CORRUPTION ("truncated
+ * file ..."), trailing bytes -> OTF_ERR_CORRUPTION, open/read failure -> OTF_ERR_IO.
+ * load_features(path, normalize) + Repository.dense — store.py:139-163, ranker.py:176-178:
+ * an empty store -> OTF_ERR_EMPTY; normalize != 0 L2-normalises every row on the device exactly as
+ * normalize_rows (store.py:32-53); a zero row -> OTF_ERR_DEGENERATE. ids are 0..count-1. */
+int otf_repo_load_dense(int device, const char* path, int normalize, otf_repo** out);
+/* load_pq_codes(path, num_centroids) + Repository.quantized — pq.py:318-330, ranker.py:180-192.
+ * centroids (num_blocks, num_centroids, subdim) float32 host; ids: count int64 or NULL. */
+int otf_repo_load_pq(int device, const char* path, const float* centroids, int32_t num_blocks,
+                     int32_t num_centroids, int32_t subdim, const int64_t* ids, otf_repo** out);
+/* load_binary_codes(path) + Repository.binary — binary.py:176-187, ranker.py:194-209.
+ * code_bytes: the codec's ceil(output_bits / 8) (0: any); out_bits receives the file's
+ * output_bits; nonzero padding bits -> OTF_ERR_CORRUPTION. */
+int otf_repo_load_binary(int device, const char* path, int32_t code_bytes, const int64_t* ids,
+                         otf_repo** out, int32_t* out_bits);
+/* The loaders' chunked, multi-threaded reads of bytes [offset, EOF) with no device copy: the
+ * host read bandwidth the loaders are measured against. */
+int otf_file_read_bench(const char* path, int64_t offset, double* seconds, int64_t* bytes_read);
 
 /* count / model_dim / payload_bytes / kind — ranker.py:213-231. */
 int otf_repo_info(const otf_repo* repo, int32_t* kind, int64_t* count, int32_t* model_dim,

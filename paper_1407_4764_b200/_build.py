@@ -21,7 +21,7 @@ LIB = PKG / "libotf_b200.so"
 OBJ = PKG / "build"
 
 SOURCES = ["otf_capi.cu", "otf_dense.cu", "otf_pq.cu", "otf_binary.cu", "otf_topk.cu", "otf_train.cu", "otf_multi.cu",
-           "otf_batch.cu", "otf_group.cu", "otf_kmeans.cu"]
+           "otf_batch.cu", "otf_group.cu", "otf_kmeans.cu", "otf_ingest.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -18,7 +18,9 @@ import numpy as np
 from .errors import (
     ConfigError,
     CorruptionError,
+    DegenerateInputError,
     EmptyStoreError,
+    FormatError,
     InsufficientDataError,
     NotReadyError,
     RetrievalError,
@@ -39,6 +41,9 @@ _ERRORS = {
     5: EmptyStoreError,
     6: RetrievalError,
     7: RetrievalError,
+    8: FormatError,
+    9: DegenerateInputError,
+    10: OSError,
 }
 
 _vp, _i64, _i32, _int, _dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_int, C.c_double
@@ -56,6 +61,10 @@ SIGNATURES: dict[str, list] = {
     "otf_repo_create_binary": [_int, _vp, _i64, _i32, _vp, _i64, _int, _int, _P(_vp)],
     "otf_repo_subset": [_vp, _vp, _i64, _P(_vp)],
     "otf_repo_destroy": [_vp],
+    "otf_repo_load_dense": [_int, C.c_char_p, _int, _P(_vp)],
+    "otf_repo_load_pq": [_int, C.c_char_p, _vp, _i32, _i32, _i32, _vp, _P(_vp)],
+    "otf_repo_load_binary": [_int, C.c_char_p, _i32, _vp, _P(_vp), _P(_i32)],
+    "otf_file_read_bench": [C.c_char_p, _i64, _P(_dbl), _P(_i64)],
     "otf_repo_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64), _P(_i32)],
     "otf_repo_score": [_vp, _vp, _vp, _int, _vp],
     "otf_repo_time_rank_scan": [_vp, _vp, _i64, _vp, _vp],

@@ -42,19 +42,6 @@ int sm_count(int device) {
   return cache[d];
 }
 
-// RAII device selection
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 // Simple device/pinned buffers ---------------------------------------------------------------
 struct DevBuf {
@@ -102,17 +89,6 @@ struct HostBuf {
 
 using namespace otf;
 
-// NVTX ranges around the public entry points (nvtx3 is header-only: a no-op unless a profiler
-// such as Nsight Systems injects itself), so a timeline shows which library call each kernel,
-// copy and synchronisation belongs to.
-#include <nvtx3/nvToolsExt.h>
-namespace {
-struct NvtxRange {
-  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
-};
-}  // namespace
-#define OTF_NVTX(name) NvtxRange _otf_nvtx_range(name)
 
 
 struct otf_repo {
@@ -255,6 +231,9 @@ int take_payload(otf_repo* r, const void* data, size_t bytes, int mem, int borro
   return copy_in(p, data, bytes, mem, r->stream);
 }
 
+}  // namespace
+void otf::repo_own_payload(otf_repo* r) { r->owns_payload = true; }
+namespace {
 void repo_free(otf_repo* r) {
   if (!r) return;
   DeviceGuard g(r->device);

@@ -1,9 +1,38 @@
 // otf_internal.h — internal launchers shared between the .cu translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
+#include "otf_b200.h"
+
 namespace otf {
+
+// RAII device selection
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// NVTX ranges around the public entry points (nvtx3 is header-only: a no-op unless a profiler
+// such as Nsight Systems injects itself), so a timeline shows which library call each kernel,
+// copy and synchronisation belongs to.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define OTF_NVTX(name) ::otf::NvtxRange _otf_nvtx_range(name)
+
+// a handle created over a borrowed device payload takes ownership of it (file loaders)
+void repo_own_payload(otf_repo* r);
 
 // Scoring launchers take the float64 model on the device and (optionally) a kHistBins-entry
 // histogram (zero on entry) that receives the coarse score histogram for launch_topk.

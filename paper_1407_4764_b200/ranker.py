@@ -12,13 +12,15 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import struct
+from pathlib import Path
 from typing import Iterator
 
 import numpy as np
 
 from . import _lib
 from .binary import binarize, unpack_bits
-from .errors import ConfigError
+from .errors import ConfigError, CorruptionError
 from .model import LinearModel, as_weights, model_version
 
 DEFAULT_LIST_SIZE = 100
@@ -141,7 +143,9 @@ class Repository:
         self.kind = kind
         self._handle = handle
         self._model_dim = int(model_dim)
-        self.ids = np.asarray(ids, dtype=np.int64)
+        # ids: an int64 array, or an int n for the implicit 0..n-1 (built on first access: a file
+        # loader's 100M-row repository does not pay an 800 MB host array it may never read)
+        self._ids = ids if isinstance(ids, int) else np.asarray(ids, dtype=np.int64)
         self.names = list(names) if names is not None else None
         self._codebook = codebook
         self._codec = codec
@@ -192,6 +196,90 @@ class Repository:
         _lib.check(lib.otf_repo_create_binary(dev, _lib.ptr(codes), codes.shape[0], bits, _lib.ptr(ids), 0,
                                               _lib.MEM_HOST, 0, C.byref(h)))
         return cls("binary", h, bits, ids, names, codec=codec, output_bits=bits)
+
+    @property
+    def ids(self) -> np.ndarray:
+        if isinstance(self._ids, int):
+            self._ids = np.arange(self._ids, dtype=np.int64)
+        return self._ids
+
+    # -- repository files straight into HBM (§8 f3; otf_ingest.cu) ------------------------------
+    @staticmethod
+    def _file_header(path, magic: bytes):
+        """(u64, u32) header fields of an OTFC / OTFH file, for the ids-length check (the C loader
+        re-validates everything, formats.py:40-84)."""
+        with open(path, "rb") as fh:  # FileNotFoundError / IsADirectoryError as the reference's open()
+            head = fh.read(20)
+        if len(head) < 20 or head[:4] != magic:
+            return None, None
+        return struct.unpack("<Q", head[8:16])[0], struct.unpack("<I", head[16:20])[0]
+
+    @classmethod
+    def load_features(cls, path, normalize: bool = True, device: int | None = None) -> "Repository":
+        """Repository.dense(load_features(path, normalize)) without a host copy of the rows:
+        store.py:139-163 (OTFR; rows L2-normalised on the device exactly as normalize_rows,
+        store.py:32-53; the ``.names`` sidecar as the reference), ranker.py:176-178."""
+        path = Path(path)
+        open(path, "rb").close()  # the reference's open() errors
+        dev = _lib.default_device() if device is None else device
+        h = C.c_void_p()
+        _lib.check(_lib.load().otf_repo_load_dense(dev, str(path).encode(), int(bool(normalize)), C.byref(h)))
+        kind, count, dim, nbytes, d = C.c_int32(), C.c_int64(), C.c_int32(), C.c_int64(), C.c_int32()
+        _lib.check(_lib.load().otf_repo_info(h, C.byref(kind), C.byref(count), C.byref(dim), C.byref(nbytes),
+                                             C.byref(d)))
+        names = None
+        names_path = path.with_suffix(path.suffix + ".names")
+        if names_path.exists():
+            names = names_path.read_text(encoding="utf-8").splitlines()
+            if len(names) != count.value:
+                _lib.load().otf_repo_destroy(h)
+                raise CorruptionError(f"{names_path}: {len(names)} names for {count.value} rows")
+        return cls("dense", h, dim.value, count.value, names)
+
+    @classmethod
+    def load_quantized(cls, codebook, path, ids=None, names=None, device: int | None = None) -> "Repository":
+        """Repository.quantized(codebook, load_pq_codes(path, codebook.num_centroids), ids, names)
+        without a host copy of the codes: pq.py:318-330 (OTFC), ranker.py:180-192."""
+        count, _ = cls._file_header(path, b"OTFC")
+        cents = np.ascontiguousarray(codebook.centroids, dtype=np.float32)
+        m, k, q = cents.shape
+        id_arr = None
+        if ids is not None:
+            id_arr = np.ascontiguousarray(ids, dtype=np.int64)
+            if count is not None and id_arr.shape != (count,):
+                raise ConfigError(f"ids shape {id_arr.shape} does not match {count} codes")
+        dev = _lib.default_device() if device is None else device
+        h = C.c_void_p()
+        _lib.check(_lib.load().otf_repo_load_pq(dev, str(path).encode(), _lib.ptr(cents), m, k, q, _lib.ptr(id_arr),
+                                                C.byref(h)))
+        ids_host = id_arr if id_arr is not None else cls._handle_count(h)
+        return cls("pq", h, m * q, ids_host, names, codebook=codebook)
+
+    @classmethod
+    def load_binary(cls, codec, path, ids=None, names=None, device: int | None = None) -> "Repository":
+        """Repository.binary(codec, load_binary_codes(path)[0], ids, names) without a host copy of
+        the codes: binary.py:176-187 (OTFH, padding bits checked on the device), ranker.py:194-209."""
+        count, _ = cls._file_header(path, b"OTFH")
+        bits = codec.frame.output_bits
+        id_arr = None
+        if ids is not None:
+            id_arr = np.ascontiguousarray(ids, dtype=np.int64)
+            if count is not None and id_arr.shape != (count,):
+                raise ConfigError(f"ids shape {id_arr.shape} does not match {count} codes")
+        dev = _lib.default_device() if device is None else device
+        h = C.c_void_p()
+        got = C.c_int32()
+        _lib.check(_lib.load().otf_repo_load_binary(dev, str(path).encode(), codec.frame.code_bytes, _lib.ptr(id_arr),
+                                                    C.byref(h), C.byref(got)))
+        ids_host = id_arr if id_arr is not None else cls._handle_count(h)
+        return cls("binary", h, bits, ids_host, names, codec=codec, output_bits=bits)
+
+    @staticmethod
+    def _handle_count(h) -> int:
+        kind, count, dim, nbytes, d = C.c_int32(), C.c_int64(), C.c_int32(), C.c_int64(), C.c_int32()
+        _lib.check(_lib.load().otf_repo_info(h, C.byref(kind), C.byref(count), C.byref(dim), C.byref(nbytes),
+                                             C.byref(d)))
+        return count.value
 
     @classmethod
     def from_device(cls, kind: str, data_ptr: int, count: int, dim: int, *, ids=None, id_base: int = 0,
