@@ -75,7 +75,7 @@ class GpuShardBackend:
         return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
 
     def to_device(self, arr):
-        return self.torch.as_tensor(arr).to(self.device, non_blocking=False)
+        return self.torch.tensor(arr, device=self.device)  # (a copy: the model's w may be read-only)
 
     def local_topk(self, w_dev, k: int):
         torch = self.torch
