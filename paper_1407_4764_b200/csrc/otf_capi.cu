@@ -537,11 +537,14 @@ int otf_repo_cut_fallbacks(otf_repo* r, int64_t* out) {
   std::lock_guard<std::mutex> lk(r->mu);
   DeviceGuard g(r->device);
   *out = 0;
-  if (!r->topk.cut_word) return OTF_OK;
   if (r->used) OTF_CUDA(cudaEventSynchronize(r->last));
-  unsigned int w = 0;
-  OTF_CUDA(cudaMemcpy(&w, r->topk.cut_word + 3, sizeof(w), cudaMemcpyDeviceToHost));
-  *out = w;
+  // the single-list cut paths (dense, PQ) and the many-classifier sampled-threshold selection
+  for (const TopkWs* ws : {&r->topk, &r->mtopk}) {
+    if (!ws->cut_word) continue;
+    unsigned int w = 0;
+    OTF_CUDA(cudaMemcpy(&w, ws->cut_word + 3, sizeof(w), cudaMemcpyDeviceToHost));
+    *out += w;
+  }
   return OTF_OK;
 }
 
@@ -746,7 +749,11 @@ int otf_repo_rank_many(otf_repo* r, const double* W, int32_t n_cls, int64_t k, i
     rc = multi_score_group(r, wp + (size_t)c0 * r->model_dim, cn, sbuf, st);
     // all cn selections in one cooperative launch (a few SMs each) when the GPU has an SM pair
     // per classifier; otherwise one launch per classifier over the whole GPU
-    if (!rc && sm_count(r->device) >= 2 * cn)
+    int seg_r = 0;
+    if (!rc && topk_seg_cut_plan(cn, r->n, k_eff, r->device, &seg_r))
+      rc = launch_topk_seg_cut(sbuf, cn, r->n, r->ids, r->id_base, k_eff, seg_r, &r->mtopk, ids + (size_t)c0 * k_eff,
+                               sc + (size_t)c0 * k_eff, r->device, st);
+    else if (!rc && sm_count(r->device) >= 2 * cn)
       rc = launch_topk_segments(sbuf, cn, r->n, r->ids, r->id_base, k_eff, &r->mtopk,
                                 ids + (size_t)c0 * k_eff, sc + (size_t)c0 * k_eff, r->device, st);
     else

@@ -137,6 +137,12 @@ int launch_topk(const void* scores, int dtype, int64_t n, const int64_t* ids, in
 // of candidates recomputed from codes + lut. scratch: n float64 (used only on the rare path).
 // n_seg independent top-k selections over consecutive float32 score arrays (scores + s*n) in one
 // cooperative launch (gridDim.x / n_seg CTAs each); outputs at out_ids/out_scores + s*k_eff.
+// The same selections by a sampled threshold per segment (otf_topk.cu topk_seg_cut_kernel): one
+// pass over the scores instead of a histogram pass and a gather pass; the plan returns false when
+// it does not apply (> 64 segments, small n, large k).
+bool topk_seg_cut_plan(int n_seg, int64_t n, int64_t k_eff, int device, int* r);
+int launch_topk_seg_cut(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff,
+                        int r, TopkWs* ws, int64_t* out_ids, double* out_scores, int device, cudaStream_t st);
 int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base,
                          int64_t k_eff, TopkWs* ws, int64_t* out_ids, double* out_scores, int device,
                          cudaStream_t st);

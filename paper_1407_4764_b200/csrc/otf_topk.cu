@@ -28,6 +28,9 @@
 #include "otf_internal.h"
 #include "otf_topk_dev.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace otf {
 
 #ifdef OTF_TOPK_TRACE  // diagnostic build (tools/): per-phase globaltimer stamps of CTAs 0 and last
@@ -426,6 +429,264 @@ int launch_topk_segments(const float* scores, int n_seg, int64_t n, const int64_
   DirectSrc<float> src{scores};
   return launch_src(src, n, ids, id_base, k_eff, ws, false, const_cast<float*>(scores), out_ids, out_scores,
                     nullptr, device, st, n_seg);
+}
+
+// ---- many selections at once, by a sampled threshold per segment (C5b's rank_many) -------------
+// n_seg independent top-k selections over consecutive float32 score arrays (scores + s * n), one
+// cooperative launch over the whole GPU:
+//   1. sample: warp w takes (segment, chunk) pairs — 64 chunks of 4096 consecutive scores spread
+//      over each segment — and publishes the chunk's four largest order keys;
+//   2. grid barrier; every CTA derives each segment's T_s = the r-th largest of its 256 published
+//      keys (r ~ (2 k + 128) x sample / n: ~2 k + 128 rows are expected at or above T_s);
+//   3. one pass over every score appends (key, ~id, row) of the scores with key >= T_s to the
+//      segment's candidate list (no histogram pass: scores concentrate in a few dozen 12-bit bins,
+//      and the segmented histogram's shared atomics serialised on them);
+//   4. grid barrier; the CTAs split into n_seg groups; a group ranks its segment's candidates by
+//      counting (rank_emit) when k <= C_s <= kCandCap, else runs the exact radix select over the
+//      segment (otf_topk_dev.cuh) — slower, same result.
+// Same order as top_k (ranker.py:97-143): the selection is exact whatever T_s is.
+constexpr int kSegSampleChunks = 64, kSegChunk = 4096, kSegPub = 4;
+
+__global__ void __launch_bounds__(kTopkThreads, kTopkCtasPerSm)
+topk_seg_cut_kernel(const float* __restrict__ scores, int n_seg, int64_t n, const int64_t* __restrict__ ids,
+                    int64_t id_base, int64_t k_eff, int r, TopkWs ws, int64_t* __restrict__ out_ids,
+                    double* __restrict__ out_scores) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ uint32_t s_T[64];
+  __shared__ uint32_t h[256];
+  __shared__ int s_b;
+  __shared__ int64_t s_above;
+  const unsigned G = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kTopkThreads / 32;
+  const int64_t gw = (int64_t)blockIdx.x * nw + wid, ngw = (int64_t)G * nw;
+  unsigned int* gbar = ws.cut_word + 12;  // the whole grid's barrier word (8-byte aligned)
+#ifdef OTF_SEG_TRACE
+  unsigned long long ts[6];
+#define SEG_STAMP(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[i]))
+#else
+#define SEG_STAMP(i)
+#endif
+  SEG_STAMP(0);
+  // 1. the sample (and the segment counters are cleared before anyone appends)
+  if (blockIdx.x == 0)
+    for (int sg = threadIdx.x; sg < n_seg; sg += blockDim.x) *seg_ws(ws, (unsigned)sg).count = 0u;
+  const int64_t stride = n / kSegSampleChunks;
+  for (int64_t t = gw; t < (int64_t)n_seg * kSegSampleChunks; t += ngw) {
+    const int sg = (int)(t / kSegSampleChunks), c = (int)(t % kSegSampleChunks);
+    const float* sp = scores + (int64_t)sg * n + (int64_t)c * stride;
+    uint32_t top[kSegPub] = {0u, 0u, 0u, 0u};  // this lane's largest keys, descending
+#pragma unroll 4
+    for (int i = lane; i < kSegChunk; i += 32) {
+      const uint32_t k = (uint32_t)score_key(__ldcg(sp + i));
+      if (k > top[3]) {
+        top[3] = k;
+#pragma unroll
+        for (int q = 3; q > 0; --q)
+          if (top[q] > top[q - 1]) { const uint32_t x = top[q]; top[q] = top[q - 1]; top[q - 1] = x; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kSegPub; ++q) {  // the warp's four largest: pop the maximum four times
+      const uint32_t m = __reduce_max_sync(0xffffffffu, top[0]);
+      const unsigned hit = __ballot_sync(0xffffffffu, top[0] == m);
+      if (lane == __ffs(hit) - 1) { top[0] = top[1]; top[1] = top[2]; top[2] = top[3]; top[3] = 0u; }
+      if (lane == 0) ws.cut_smax[((int64_t)sg * kSegSampleChunks + c) * kSegPub + q] = m;
+    }
+  }
+  SEG_STAMP(1);
+  grid_barrier(gbar, G);
+  SEG_STAMP(2);
+  // 2. T_s for every segment (each warp: segments wid, wid + nw; 256 keys, 8 per lane): the r-th
+  // largest at 16-bit key resolution (two 8-bit radix passes over a per-warp shared histogram),
+  // rounded down to that prefix's lower edge
+  {
+    uint32_t* wh = reinterpret_cast<uint32_t*>(dyn) + wid * 256;
+    for (int sg = wid; sg < n_seg; sg += nw) {
+      uint32_t v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(ws.cut_smax + (int64_t)sg * 256 + lane + 32 * q);
+      uint32_t prefix = 0, T = 0;
+      int need = r;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int shift = 24 - 8 * pass;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) wh[lane + 32 * q] = 0u;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (v[q] != 0u && (pass == 0 || (v[q] >> 24) == prefix)) atomicAdd(&wh[(v[q] >> shift) & 255u], 1u);
+        __syncwarp();
+        // lane l owns bins 255 - 8 l - 7 .. 255 - 8 l (descending); the bin holding the need-th key
+        uint32_t c[8];
+        int local = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c[q] = wh[255 - 8 * lane - q]; local += (int)c[q]; }
+        int incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot < need) { T = 0u; break; }  // fewer than r sampled keys: the segment falls back
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
+        const int first = __ffs(hit) - 1;
+        int bin = 0, above = 0;
+        if (lane == first) {
+          int cum = incl - local;
+          for (int q = 0; q < 8; ++q) {
+            if (cum + (int)c[q] >= need) { bin = 255 - 8 * lane - q; above = cum; break; }
+            cum += (int)c[q];
+          }
+        }
+        bin = __shfl_sync(0xffffffffu, bin, first);
+        above = __shfl_sync(0xffffffffu, above, first);
+        need -= above;
+        prefix = pass == 0 ? (uint32_t)bin : (prefix << 8) | (uint32_t)bin;
+        if (pass == 1) T = prefix << 16;
+        __syncwarp();
+      }
+      if (lane == 0) s_T[sg] = T;
+    }
+  }
+  __syncthreads();
+  SEG_STAMP(3);
+  // 3. emission: lane l of a warp takes two float4 (flat positions 4 l and 128 + 4 l of a 256-score
+  // run); a take is rare (~0.02% of the scores), so one comparison per float4 decides
+  const int64_t total = (int64_t)n_seg * n;
+  auto emit = [&](int64_t f, float sc) {  // f: flat position of a score at or above its T
+    const int sg = (int)(f / n);
+    const int64_t row = f - (int64_t)sg * n;
+    const TopkWs w = seg_ws(ws, (unsigned)sg);
+    const unsigned slot = atomicAdd(w.count, 1u);
+    if ((int64_t)slot < w.cap) {
+      w.key[slot] = score_key(sc);
+      w.inv[slot] = inv_id(id_of(ids, id_base, row));
+      w.row[slot] = row;
+    }
+  };
+  auto test4 = [&](int64_t f, float4 x, int cnt) {  // cnt valid scores from f
+    const int sg = (int)(f / n);
+    const int64_t bnd = (int64_t)(sg + 1) * n;  // the next segment starts here
+    const uint32_t T0 = s_T[sg], T1 = bnd < f + cnt && sg + 1 < n_seg ? s_T[sg + 1] : T0;
+    const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q >= cnt) break;
+      const uint32_t T = f + q < bnd ? T0 : T1;
+      if (T != 0u && (uint32_t)score_key(xs[q]) >= T) emit(f + q, xs[q]);
+    }
+  };
+  const bool aligned = (reinterpret_cast<uintptr_t>(scores) & 15) == 0;
+  constexpr int kRuns = 8;  // float4 per lane in flight (1024 scores per warp iteration)
+  for (int64_t f0 = gw * (128 * kRuns); f0 < total; f0 += ngw * (128 * kRuns)) {
+    // the warp's run two iterations ahead streams into L2 meanwhile (one bulk prefetch): the
+    // loads below then wait on L2, not HBM (32 warps x 4 KB in flight per SM is not enough)
+    if (lane == 0 && aligned) {
+      const int64_t fp = f0 + 2 * ngw * (128 * kRuns);
+      if (fp + 128 * kRuns <= total)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scores + fp), "r"(512u * kRuns) : "memory");
+    }
+    float4 x[kRuns];
+#pragma unroll
+    for (int h = 0; h < kRuns; ++h) {
+      const int64_t f = f0 + 128 * h + 4 * lane;
+      if (f + 4 <= total && aligned) {
+        x[h] = ld_stream_f4(reinterpret_cast<const float4*>(scores + f));  // (256 B L2 fetches, evict-first)
+      } else {
+        x[h].x = f < total ? __ldcs(scores + f) : 0.f;
+        x[h].y = f + 1 < total ? __ldcs(scores + f + 1) : 0.f;
+        x[h].z = f + 2 < total ? __ldcs(scores + f + 2) : 0.f;
+        x[h].w = f + 3 < total ? __ldcs(scores + f + 3) : 0.f;
+      }
+    }
+    // one division per 1024 scores: a run spans at most two segments (n >= 1M, topk_seg_cut_plan)
+    const int sg0 = (int)(f0 / n);
+    const int64_t bnd0 = (int64_t)(sg0 + 1) * n;
+#pragma unroll
+    for (int h = 0; h < kRuns; ++h) {
+      const int64_t f = f0 + 128 * h + 4 * lane;
+      if (f >= total) continue;
+      const int cnt = (int)min((int64_t)4, total - f);
+      // quick reject: the largest key of the four against the smaller of the (at most two) T's
+      const int sg = f < bnd0 ? sg0 : sg0 + 1;
+      const uint32_t t0 = s_T[sg] ? s_T[sg] : 0xffffffffu;
+      const uint32_t t1 = sg + 1 < n_seg && (int64_t)(sg + 1) * n < f + cnt ? (s_T[sg + 1] ? s_T[sg + 1] : 0xffffffffu)
+                                                                           : 0xffffffffu;
+      const uint32_t kmax = max(max((uint32_t)score_key(x[h].x), cnt > 1 ? (uint32_t)score_key(x[h].y) : 0u),
+                                max(cnt > 2 ? (uint32_t)score_key(x[h].z) : 0u, cnt > 3 ? (uint32_t)score_key(x[h].w) : 0u));
+      if (kmax >= min(t0, t1)) test4(f, x[h], cnt);
+    }
+  }
+  SEG_STAMP(4);
+  grid_barrier(gbar, G);
+  SEG_STAMP(5);
+#ifdef OTF_SEG_TRACE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1))
+    printf("segT cta %d sample %.1f barrier %.1f T %.1f emit %.1f barrier %.1f us\n", (int)blockIdx.x,
+           (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3,
+           (ts[5] - ts[4]) * 1e-3);
+#endif
+  // 4. per-segment groups of G / n_seg CTAs: rank the candidates, or the exact select
+  const unsigned per = G / (unsigned)n_seg;
+  const unsigned sg = blockIdx.x / per, vb = blockIdx.x % per;
+  if (sg >= (unsigned)n_seg) return;
+  const TopkWs w = seg_ws(ws, sg);
+  const unsigned C = __ldcg(w.count);
+  DirectSrc<float> src{scores + (int64_t)sg * n};
+  if (s_T[sg] != 0u && (int64_t)C >= k_eff && C <= (unsigned)kCandCap) {
+    rank_emit(src, w, (int64_t)C, k_eff, dyn, out_ids + (int64_t)sg * k_eff, out_scores + (int64_t)sg * k_eff, nullptr,
+              vb, per);
+    grid_barrier(w.bar, per);  // (the other path's kernels expect a zero count)
+    if (vb == 0 && threadIdx.x == 0) *w.count = 0u;
+    return;
+  }
+  if (vb == 0 && threadIdx.x == 0) atomicAdd(ws.cut_word + 3, 1u);  // fallbacks taken (diagnostics)
+  grid_barrier(w.bar, per);  // the group's CTAs have read the count
+  if (vb == 0 && threadIdx.x == 0) *w.count = 0u;
+  grid_barrier(w.bar, per);
+  radix_select_emit(src.s, src, n, ids, id_base, k_eff, w, k_eff >= n, dyn, out_ids + (int64_t)sg * k_eff,
+                    out_scores + (int64_t)sg * k_eff, nullptr, h, &s_b, &s_above, vb, per);
+}
+
+bool topk_seg_cut_plan(int n_seg, int64_t n, int64_t k_eff, int device, int* r) {
+  static const bool off = getenv("OTF_SEG_NO_CUT") != nullptr;  // A/B switch (tools/)
+  if (off || n_seg < 1 || n_seg > 64 || k_eff <= 0) return false;
+  if (sm_count(device) / n_seg < 1) return false;
+  const int64_t S = (int64_t)kSegSampleChunks * kSegChunk;
+  if (n < 4 * S) return false;  // the sample is at most a quarter of a segment
+  const int64_t want = 2 * k_eff + 128;
+  if (2 * want > kCandCap) return false;
+  const int64_t rr = (want * S + n - 1) / n;
+  if (rr > kSegSampleChunks * kSegPub / 4) return false;  // the published keys must cover the top r
+  *r = (int)std::max<int64_t>(rr, 1);
+  return true;
+}
+
+int launch_topk_seg_cut(const float* scores, int n_seg, int64_t n, const int64_t* ids, int64_t id_base, int64_t k_eff,
+                        int r, TopkWs* ws, int64_t* out_ids, double* out_scores, int device, cudaStream_t st) {
+  int rc = topk_ws_alloc(ws, k_eff, n_seg);
+  if (!rc) rc = topk_cut_alloc(ws);
+  if (rc) return rc;
+  auto fn = topk_seg_cut_kernel;
+  static bool configured[64] = {false};
+  if (!configured[device & 63]) {
+    OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkSmem));
+    configured[device & 63] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(sm_count(device) * kTopkCtasPerSm));
+  cfg.blockDim = dim3(kTopkThreads);
+  cfg.dynamicSmemBytes = kTopkSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, scores, n_seg, n, ids, id_base, k_eff, r, *ws, out_ids, out_scores));
+  count_launch();
+  return OTF_OK;
 }
 
 int launch_topk_pq_bins(const uint16_t* bins, const uint8_t* codes, int M, const double* lut, int K,

@@ -195,3 +195,26 @@ def test_rank_many_unaligned_segments(otf, n, c):
         o_ids, o_sc, _ = O.top_k(S[i], k)
         np.testing.assert_array_equal(lists[i].ids, o_ids)
         np.testing.assert_array_equal(lists[i].scores, o_sc)
+
+
+@pytest.mark.parametrize("n,c,k", [(1_100_003, 64, 1000), (1_048_576, 9, 1), (2_000_000, 33, 700)])
+def test_rank_many_sampled_threshold(otf, n, c, k):
+    """Segments of >= 1M rows take the sampled-threshold selection (topk_seg_cut_kernel: a sample
+    per classifier, one emission pass, rank by counting): lists equal the oracle's top_k of the
+    scores, with a zero classifier (every row reaches T -> that segment's exact radix select), a
+    tie-heavy one, shuffled ids and unaligned segment starts; a following k beyond the plan (the
+    histogram path, same workspace) is unaffected."""
+    rng = np.random.default_rng(n + c + k)
+    x = np.round(rng.standard_normal((n, 64)) * 8).astype(np.float32) / 8
+    ids = rng.permutation(2 * n)[:n].astype(np.int64)
+    W = rng.standard_normal((c, 64))
+    W[0] = 0.0
+    W[c // 2] = np.round(W[c // 2])
+    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    S = repo.score_many(list(W))
+    for kk in (k, 3000):
+        lists = repo.rank_many([otf.LinearModel(w, 1, 1) for w in W], kk)
+        for i in range(c):
+            o_ids, o_sc, _ = O.top_k(S[i], kk, ids)
+            np.testing.assert_array_equal(lists[i].ids, o_ids)
+            np.testing.assert_array_equal(lists[i].scores, o_sc)
