@@ -143,6 +143,12 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
 // Measured (B200, same box): C2 (1M x 2048) 1167 vs 1180 us per query for scan + top-k kernel;
 // C1 (1M x 128) 101.0 vs 98.9 us — at 14 warp iterations per warp the scan's finishing spread
 // (51-66 us between CTAs) costs what the top-k kernel did, so d = 128 keeps the two-kernel path.
+#ifndef OTF_DC_TAIL_DIV  // 1 / OTF_DC_TAIL_DIV of the groups are handed out dynamically
+#define OTF_DC_TAIL_DIV 4
+#endif
+#ifndef OTF_DC_CLAIM  // groups per claim of the dynamic tail
+#define OTF_DC_CLAIM 4
+#endif
 constexpr int kDcThreads = 256;
 constexpr int kDcSelCap = 5120;  // candidates ranked in shared memory (32-bit keys)
 constexpr int kDcFallbackK = 1280;  // the radix fallback ranks k (key, inv) pairs in the same memory
@@ -314,12 +320,36 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
     if (usable) emit(own && (uint32_t)score_key(held[h2]) >= tkey, held[h2], row);
     else if (own) scratch[row] = held[h2];  // the fallback needs every score
   }
-  for (; gcur < ngroups; gcur = next_group(gcur + nwarp)) {  // warp-uniform
-    const float s = dense_iter<CPL, R>(X4, n, gcur * R, wr, lane);
-    const int64_t row = gcur * R + slot;
+  auto process = [&](int64_t g) {
+    const float s = dense_iter<CPL, R>(X4, n, g * R, wr, lane);
+    const int64_t row = g * R + slot;
     const bool own = writer && row < n;
     if (usable) emit(own && (uint32_t)score_key(s) >= tkey, s, row);
     else if (own) scratch[row] = s;
+  };
+  // the first 3/4 of the groups interleaved as dense_score_fast (static) ...
+  const int64_t gstat = (ngroups - ngroups / OTF_DC_TAIL_DIV) / nwarp * nwarp;
+  for (; gcur < gstat; gcur = next_group(gcur + nwarp)) process(gcur);  // warp-uniform
+  // ... the last 1/4 handed out four groups at a time by four counters (warp & 3 serves the tail
+  // groups congruent to it mod 4): SMs that stream faster take more of it, so every CTA reaches
+  // the barrier within about one claim of the others (the static split left a 130 us spread
+  // between CTAs on C2). Swept on B200 (tail 1/16..1/2, 1..4 groups per claim): C2 1.177 ->
+  // 1.117 ms, C4 7.23 -> 6.90 ms per query; one group per claim contends on the counters.
+  {
+    const int c = (int)(warp & 3);
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws.cut_word + 8 + 2 * c);
+    for (;;) {
+      unsigned long long j0 = 0;
+      if (lane == 0) j0 = atomicAdd(ctr, (unsigned long long)OTF_DC_CLAIM);
+      j0 = __shfl_sync(0xffffffffu, j0, 0);
+      const int64_t g0 = gstat + 4 * (int64_t)j0 + c;
+      if (g0 >= ngroups) break;
+#pragma unroll 1
+      for (int u = 0; u < OTF_DC_CLAIM; ++u) {
+        const int64_t g = g0 + 4 * u;
+        if (g < ngroups && !is_sample(g)) process(g);
+      }
+    }
   }
   DC_STAMP(3);
   grid_barrier(ws.bar, G);  // every candidate record is in place
@@ -335,6 +365,7 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
     s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
     if (s_last) {
       ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[6] = 0u;
+      for (int q = 8; q < 16; ++q) ws.cut_word[q] = 0u;  // the tail's claim counters
     }
   }
   if (ok) {
