@@ -274,9 +274,16 @@ int stage_w(otf_repo* r, const double* w, int mem, cudaStream_t st, const double
 int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStream_t st,
                uint16_t* cmax = nullptr, int* clog = nullptr) {
   int rc = OTF_OK;
-  if (r->kind == OTF_KIND_DENSE)
+  if (r->kind == OTF_KIND_DENSE) {
+    // the rank path (hist) hands the scan's tail out dynamically (counters in the cut words)
+    unsigned int* claim = nullptr;
+    if (hist) {
+      if ((rc = topk_cut_alloc(&r->topk))) return rc;
+      claim = r->topk.cut_word + kCutClaimWord;
+    }
     return launch_dense_score(static_cast<const float*>(r->payload), r->n, r->model_dim, dw,
-                              static_cast<float*>(out), hist, r->device, st, cmax, clog);
+                              static_cast<float*>(out), hist, r->device, st, cmax, clog, claim);
+  }
   if (r->kind == OTF_KIND_PQ) {
     // the (M, K) float64 LUT is built once per query (one thread per entry), then every scan
     // CTA copies it into shared memory instead of re-deriving it

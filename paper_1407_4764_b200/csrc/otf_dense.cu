@@ -85,12 +85,17 @@ __device__ __forceinline__ void stage_w(const double* __restrict__ w, float4* wr
 }
 
 // Fast path: d == 128 * CPL, every row's score (+ the fused histogram / chunk maxima).
+// claim (nullable): 10 words {4 u64 tail counters, done ticket, pad} zero on entry, left zero. With
+// it the last quarter of the groups is handed out dynamically, 4 groups per claim, by 4 counters
+// (as dense_rank_cut's tail), so faster SMs take more and the kernel ends within ~one claim of
+// its mean; without it (score(), no workspace) every group is assigned statically.
 template <int CPL, int R>
 __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restrict__ X, int64_t n,
                                                            const double* __restrict__ w,
                                                            float* __restrict__ out,
                                                            uint32_t* __restrict__ ghist,
-                                                           uint16_t* __restrict__ cmax) {
+                                                           uint16_t* __restrict__ cmax,
+                                                           unsigned int* __restrict__ claim) {
   const int lane = threadIdx.x & 31;
   __shared__ float4 wr[32 * CPL];
   __shared__ uint32_t sh[kHistBins];
@@ -100,7 +105,9 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
   const float4* X4 = reinterpret_cast<const float4*>(X);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
+  const int64_t ngroups = (n + R - 1) / R;
+  auto group = [&](int64_t g) {
+    const int64_t r0 = g * R;
     const float s = dense_iter<CPL, R>(X4, n, r0, wr, lane);
     bool writer;
     const int slot = row_of_lane<R, 32>(lane, &writer);
@@ -110,7 +117,44 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
     if (ghist) hist_add(sh, active, hist_bin(s));
     if (R > 1 && cmax) {  // the warp's R consecutive rows are one top-k chunk
       const uint32_t wm = __reduce_max_sync(0xffffffffu, active ? hist_bin(s) : 0u);
-      if (lane == 0) cmax[r0 / R] = (uint16_t)wm;
+      if (lane == 0) cmax[g] = (uint16_t)wm;
+    }
+  };
+  const int64_t gstat = claim ? (ngroups - ngroups / 4) / nwarp * nwarp : ngroups;
+  // one loop (one inlined copy of the scan): static groups warp, warp + nwarp, ... below gstat,
+  // then tail groups gstat + 4 j + (warp & 3) for j claimed four at a time
+  const int c = (int)(warp & 3);
+  unsigned long long* ctr = claim ? reinterpret_cast<unsigned long long*>(claim) + c : nullptr;
+  int64_t j = 0;
+  int left = 0;
+  auto tail = [&]() -> int64_t {
+    if (!claim) return ngroups;
+    if (left == 0) {
+      unsigned long long j0 = 0;
+      if (lane == 0) j0 = atomicAdd(ctr, 4ull);
+      j = (int64_t)__shfl_sync(0xffffffffu, j0, 0);
+      left = 4;
+    } else {
+      ++j;
+    }
+    --left;
+    const int64_t g = gstat + 4 * j + c;
+    return g < ngroups ? g : ngroups;
+  };
+  for (int64_t g = warp < gstat ? warp : tail(); g < ngroups;) {  // warp-uniform
+    group(g);
+    g += nwarp;
+    if (g >= gstat) g = tail();
+  }
+  if (claim) {
+    // the last CTA out clears the counters for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(claim + 8, 1u) == gridDim.x - 1) {
+        for (int q = 0; q < 9; ++q) claim[q] = 0u;
+        __threadfence();
+      }
     }
   }
   if (ghist) {
@@ -470,13 +514,13 @@ static int grid_for(const void* fn, int threads, int device) {
 
 template <int CPL, int R>
 static int launch_fast(const float* X, int64_t n, const double* w, float* out, uint32_t* hist,
-                       int device, cudaStream_t st, uint16_t* cmax, int* clog) {
+                       int device, cudaStream_t st, uint16_t* cmax, int* clog, unsigned int* claim) {
   auto fn = dense_score_fast<CPL, R>;
   int grid = grid_for((const void*)fn, 256, device);
   const int64_t need = (n + (8 * R) - 1) / (8 * R);  // 8 warps per block
   if (need < grid) grid = (int)(need > 0 ? need : 1);
   if (R < 8) cmax = nullptr;  // chunks of >= 8 rows only (topk_cmax_ensure)
-  fn<<<grid, 256, 0, st>>>(X, n, w, out, hist, cmax);
+  fn<<<grid, 256, 0, st>>>(X, n, w, out, hist, cmax, claim);
   OTF_LAUNCH_CHECK("dense_score_fast");
   if (cmax && clog) *clog = R == 8 ? 3 : R == 16 ? 4 : 5;  // log2(R)
   return OTF_OK;
@@ -579,17 +623,20 @@ int launch_dense_rank_cut(const float* X, int64_t n, int32_t d, const double* w,
 // 16-byte aligned for the fast path (all device buffers this library allocates are).
 // hist (nullable): kHistBins counters (zero on entry) receiving the coarse score histogram.
 int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
-                       uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax, int* clog) {
+                       uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax, int* clog,
+                       unsigned int* claim) {
+  static const bool no_tail = getenv("OTF_DENSE_STATIC") != nullptr;  // A/B switch (tools/)
+  if (no_tail) claim = nullptr;
   if (n <= 0) return OTF_OK;
   const bool aligned = (((uintptr_t)X) & 15) == 0;
   if (aligned && d % 128 == 0) {
     switch (d / 128) {
-      case 1: return launch_fast<1, 32>(X, n, w, out, hist, device, st, cmax, clog);  // R 8/16: 5% slower (C1)
-      case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st, cmax, clog);
-      case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st, cmax, clog);
-      case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st, cmax, clog);
-      case 16: return launch_fast<16, 2>(X, n, w, out, hist, device, st, cmax, clog);  // R 1 / 4: +0.6% / +2.8%
-      case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st, cmax, clog);
+      case 1: return launch_fast<1, 32>(X, n, w, out, hist, device, st, cmax, clog, claim);  // R 8/16: 5% slower (C1)
+      case 2: return launch_fast<2, 4>(X, n, w, out, hist, device, st, cmax, clog, claim);
+      case 4: return launch_fast<4, 2>(X, n, w, out, hist, device, st, cmax, clog, claim);
+      case 8: return launch_fast<8, 1>(X, n, w, out, hist, device, st, cmax, clog, claim);
+      case 16: return launch_fast<16, 2>(X, n, w, out, hist, device, st, cmax, clog, claim);  // R 1 / 4: +0.6% / +2.8%
+      case 32: return launch_fast<32, 1>(X, n, w, out, hist, device, st, cmax, clog, claim);
       default: break;
     }
   }

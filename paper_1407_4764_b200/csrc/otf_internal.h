@@ -40,9 +40,11 @@ void repo_own_payload(otf_repo* r);
 // dense (otf_dense.cu)
 // cmax (nullable): per-chunk maximum score bins for the top-k gather; *clog is set to log2 of
 // the chunk size when the kernel wrote them, else left at -1.
+// claim (nullable): 10 zeroed words; the last quarter of the rows is then handed out dynamically
+// (dense_score_fast), and the words are left zero
 int launch_dense_score(const float* X, int64_t n, int32_t d, const double* w, float* out,
                        uint32_t* hist, int device, cudaStream_t st, uint16_t* cmax = nullptr,
-                       int* clog = nullptr);
+                       int* clog = nullptr, unsigned int* claim = nullptr);
 
 // fused dense rank (score + exact top-k, one cooperative launch; otf_dense.cu dense_rank_cut).
 // dense_cut_plan returns false when the path does not apply (unaligned / unsupported d, large k,
@@ -123,6 +125,10 @@ struct TopkWs {
 constexpr int64_t kCutCap = 1 << 16;
 constexpr int kCutSampleCtasMax = 1024;
 constexpr int kCutSmaxCap = 16384;
+// cut_word: [0..15] the fused selections' counters and barrier words, [16..25] the dynamic tail
+// of dense_score_fast (launch_dense_score's claim), all zero between launches
+constexpr int kCutWords = 32;
+constexpr int kCutClaimWord = 16;
 int topk_cut_alloc(TopkWs* ws);
 // ensures ws->cmax holds the chunk maxima of n rows for chunks of >= 8 rows (zero padded)
 int topk_cmax_ensure(TopkWs* ws, int64_t n);

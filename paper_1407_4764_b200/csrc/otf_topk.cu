@@ -314,8 +314,8 @@ int topk_cut_alloc(TopkWs* ws) {
   if (ws->cut_cap >= kCutCap) return OTF_OK;
   OTF_CUDA(cudaMalloc(&ws->cut_key, 2 * kCutCap * sizeof(uint64_t)));  // (key, ~id) records
   OTF_CUDA(cudaMalloc(&ws->cut_row, kCutCap * sizeof(int64_t)));
-  OTF_CUDA(cudaMalloc(&ws->cut_word, 16 * sizeof(unsigned int)));
-  OTF_CUDA(cudaMemset(ws->cut_word, 0, 16 * sizeof(unsigned int)));
+  OTF_CUDA(cudaMalloc(&ws->cut_word, kCutWords * sizeof(unsigned int)));
+  OTF_CUDA(cudaMemset(ws->cut_word, 0, kCutWords * sizeof(unsigned int)));
   OTF_CUDA(cudaMalloc(&ws->cut_smax, kCutSmaxCap * sizeof(uint32_t)));
   ws->cut_cap = kCutCap;
   return OTF_OK;
