@@ -296,6 +296,8 @@ int score_into(otf_repo* r, const double* dw, void* out, uint32_t* hist, cudaStr
   }
   // multi-slice byte-table path chains a float64 partial per row
   if ((rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * sizeof(double)))) return rc;
+  // (a dynamic tail as the dense scans' measured no faster here: the byte-table scan is LSU-bound,
+  // not unbalanced — C5a 5.94-5.99 vs 5.91-5.97 ms on the same box)
   return launch_bin_score(static_cast<const uint8_t*>(r->payload), r->n, r->model_dim, dw,
                           static_cast<float*>(out), hist, static_cast<double*>(r->bins.p), r->device,
                           st, cmax, clog);
@@ -799,7 +801,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
   if (!rc && (r->kind == OTF_KIND_PQ)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 2);
   if (!rc && (r->kind == OTF_KIND_BINARY)) rc = r->bins.ensure((size_t)(r->n > 0 ? r->n : 1) * 8);
   if (!rc) rc = topk_cmax_ensure(&r->topk, r->n);
-  if (!rc && (r->kind == OTF_KIND_PQ || r->kind == OTF_KIND_DENSE)) rc = topk_cut_alloc(&r->topk);
+  if (!rc) rc = topk_cut_alloc(&r->topk);  // (every kind: the fused paths' words, the scans' dynamic tails)
   if (rc) return rc;
   if (r->kind == OTF_KIND_DENSE) {  // the plan's one-time kernel attributes, outside the capture
     DenseCutPlan dpl;
