@@ -99,6 +99,9 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
   const int lane = threadIdx.x & 31;
   __shared__ float4 wr[32 * CPL];
   __shared__ uint32_t sh[kHistBins];
+  // the top-k kernel (programmatic launch) may be scheduled now: its CTAs take SMs as this grid's
+  // CTAs finish and wait in griddepcontrol.wait for this grid's writes
+  asm volatile("griddepcontrol.launch_dependents;");
   stage_w<CPL>(w, wr);
   if (ghist) hist_zero(sh);
   __syncthreads();

@@ -78,6 +78,9 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
   __shared__ int64_t wsum[32];
   const unsigned int nb = vnb;
   const int lane = threadIdx.x & 31;
+  // launched programmatically after the scoring kernel (hist_ready): the CTAs come up while its
+  // last CTAs drain, and wait here for its scores / histogram / chunk maxima (a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t nthreads = (int64_t)vnb * blockDim.x;
   const int64_t wbase0 = (int64_t)vb * blockDim.x + (threadIdx.x & ~31);
   const bool all = k_eff >= n;
@@ -391,11 +394,14 @@ static int launch_src(const Src& src, int64_t n, const int64_t* ids, int64_t id_
   cfg.blockDim = dim3(kTopkThreads);
   cfg.dynamicSmemBytes = kTopkSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // follows the fused scoring kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool no_pdl = getenv("OTF_TOPK_NO_PDL") != nullptr;  // A/B switch (tools/)
+  cfg.numAttrs = hist_ready && !no_pdl ? 2 : 1;
   OTF_CUDA(cudaLaunchKernelEx(&cfg, fn, src, n, ids, id_base, k_eff, *ws, (int)hist_ready, scratch,
                               out_ids, out_scores, out_rows, n_seg));
   count_launch();
