@@ -187,15 +187,18 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
 //      far off the distribution) every row's score is written to `scratch` and the exact radix
 //      select (otf_topk_dev.cuh) runs — slower, same result.
 // Order: (score desc, id asc), -0.0 tied with +0.0, the row as the last tie key (ranker.py:97-143).
-// Measured (B200, same box): C2 (1M x 2048) 1167 vs 1180 us per query for scan + top-k kernel;
-// C1 (1M x 128) 101.0 vs 98.9 us — at 14 warp iterations per warp the scan's finishing spread
-// (51-66 us between CTAs) costs what the top-k kernel did, so d = 128 keeps the two-kernel path.
+// Measured (B200, same box): C2 (1M x 2048) 1.117 vs 1.177 ms per query for scan + top-k
+// kernel; C4 6.87 vs 7.23 ms; C1 (1M x 128) 96.6-97.4 vs 99.2 us.
 #ifndef OTF_DC_TAIL_DIV  // 1 / OTF_DC_TAIL_DIV of the groups are handed out dynamically
 #define OTF_DC_TAIL_DIV 4
 #endif
 #ifndef OTF_DC_CLAIM  // groups per claim of the dynamic tail
-#define OTF_DC_CLAIM 4
+#define OTF_DC_CLAIM 1
 #endif
+#ifndef OTF_DC_CTRS  // claim counters of the dynamic tail (<= 16, one cache line each)
+#define OTF_DC_CTRS 16
+#endif
+constexpr int kDcCtrWord = 64, kDcCtrStride = 32;  // tail counter c: cut words 64 + 32 c (one 128-byte line each)
 constexpr int kDcThreads = 256;
 constexpr int kDcSelCap = 5120;  // candidates ranked in shared memory (32-bit keys)
 constexpr int kDcFallbackK = 1280;  // the radix fallback ranks k (key, inv) pairs in the same memory
@@ -377,23 +380,26 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
   // the first 3/4 of the groups interleaved as dense_score_fast (static) ...
   const int64_t gstat = (ngroups - ngroups / OTF_DC_TAIL_DIV) / nwarp * nwarp;
   for (; gcur < gstat; gcur = next_group(gcur + nwarp)) process(gcur);  // warp-uniform
-  // ... the last 1/4 handed out four groups at a time by four counters (warp & 3 serves the tail
-  // groups congruent to it mod 4): SMs that stream faster take more of it, so every CTA reaches
-  // the barrier within about one claim of the others (the static split left a 130 us spread
-  // between CTAs on C2). Swept on B200 (tail 1/16..1/2, 1..4 groups per claim): C2 1.177 ->
-  // 1.117 ms, C4 7.23 -> 6.90 ms per query; one group per claim contends on the counters.
+  // ... the last 1/4 handed out one group at a time by 16 counters (warp % 16 serves the tail
+  // groups congruent to it mod 16; each counter on its own 128-byte line; the next claim is
+  // requested while the current group is scored): SMs that stream faster take more of it, so
+  // every CTA reaches the barrier within about one group of the others (the static split left a
+  // 130 us spread between CTAs on C2). Swept on B200: C2 1.177 -> 1.117 ms, C4 7.23 -> 6.87 ms,
+  // C1 (fused) 101.5 -> 97 us; with the counters on ONE cache line, single-group claims
+  // serialised on it (C4 7.76 ms) and 4-group claims were best (6.90 ms).
   {
-    const int c = (int)(warp & 3);
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws.cut_word + 8 + 2 * c);
+    const int c = (int)(warp % OTF_DC_CTRS);
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws.cut_word + kDcCtrWord + kDcCtrStride * c);
+    unsigned long long jn = 0;  // the next claim, requested one claim ahead (latency hidden)
+    if (lane == 0) jn = atomicAdd(ctr, (unsigned long long)OTF_DC_CLAIM);
     for (;;) {
-      unsigned long long j0 = 0;
-      if (lane == 0) j0 = atomicAdd(ctr, (unsigned long long)OTF_DC_CLAIM);
-      j0 = __shfl_sync(0xffffffffu, j0, 0);
-      const int64_t g0 = gstat + 4 * (int64_t)j0 + c;
+      const unsigned long long j0 = __shfl_sync(0xffffffffu, jn, 0);
+      const int64_t g0 = gstat + OTF_DC_CTRS * (int64_t)j0 + c;
       if (g0 >= ngroups) break;
+      if (lane == 0) jn = atomicAdd(ctr, (unsigned long long)OTF_DC_CLAIM);
 #pragma unroll 1
       for (int u = 0; u < OTF_DC_CLAIM; ++u) {
-        const int64_t g = g0 + 4 * u;
+        const int64_t g = g0 + OTF_DC_CTRS * u;
         if (g < ngroups && !is_sample(g)) process(g);
       }
     }
@@ -412,7 +418,10 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
     s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
     if (s_last) {
       ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[6] = 0u;
-      for (int q = 8; q < 16; ++q) ws.cut_word[q] = 0u;  // the tail's claim counters
+      for (int q = 0; q < OTF_DC_CTRS; ++q) {  // the tail counters
+        ws.cut_word[kDcCtrWord + kDcCtrStride * q] = 0u;
+        ws.cut_word[kDcCtrWord + kDcCtrStride * q + 1] = 0u;
+      }
     }
   }
   if (ok) {
@@ -584,8 +593,6 @@ bool dense_cut_plan(int32_t d, const float* X, int64_t n, int64_t k_eff, int dev
   static const bool off = getenv("OTF_DENSE_NO_CUT") != nullptr;  // A/B switch (tools/)
   if (off || k_eff <= 0 || d % 128 != 0 || (((uintptr_t)X) & 15) != 0) return false;
   const int cpl = d / 128;
-  static const bool d128 = getenv("OTF_DENSE_CUT_D128") != nullptr;  // A/B switch (tools/)
-  if (cpl == 1 && !d128) return false;  // measured slower at d = 128 (see dense_rank_cut)
   if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && cpl != 16 && cpl != 32) return false;
   // ~2 k + 128 candidates are expected; their count must stay well inside the shared-memory cap
   const int64_t want = 2 * k_eff + 128;

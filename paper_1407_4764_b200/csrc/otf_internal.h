@@ -126,8 +126,9 @@ constexpr int64_t kCutCap = 1 << 16;
 constexpr int kCutSampleCtasMax = 1024;
 constexpr int kCutSmaxCap = 16384;
 // cut_word: [0..15] the fused selections' counters and barrier words, [16..25] the dynamic tail
-// of dense_score_fast (launch_dense_score's claim), all zero between launches
-constexpr int kCutWords = 32;
+// of dense_score_fast (launch_dense_score's claim), [64 + 32 c] dense_rank_cut's tail counter c
+// (one 128-byte line each, c < 16), all zero between launches
+constexpr int kCutWords = 64 + 16 * 32;
 constexpr int kCutClaimWord = 16;
 int topk_cut_alloc(TopkWs* ws);
 // ensures ws->cmax holds the chunk maxima of n rows for chunks of >= 8 rows (zero padded)

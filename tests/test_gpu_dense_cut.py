@@ -38,7 +38,7 @@ def check(otf, repo, w, k, ids=None):
     return r
 
 
-D, N, R = 256, 600_000, 4  # (d = 128 takes the two-kernel path: dense_cut_plan)
+D, N, R = 256, 600_000, 4
 
 
 @pytest.fixture(scope="module")

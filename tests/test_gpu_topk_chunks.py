@@ -3,7 +3,8 @@ gather reads the per-chunk maximum bins the scoring kernel wrote and scans only 
 can hold a candidate. The selection must stay exactly the oracle's top_k (ranker.py:97-143) of
 the GPU's own scores: heavy ties at the threshold bin spread over many chunks, a partial last
 chunk, ids in shuffled order, k up to the 8192-candidate cap and beyond (radix-select fallback),
-and all three chunk sizes (dense d=128: 32 rows, binary 2048-bit: 32, PQ-16: 128).
+and all three chunk sizes (dense d=128: 32 rows — the two-kernel path for k beyond the fused
+selection's cap, the fused dense_rank_cut below it —, binary 2048-bit: 32, PQ-16: 128).
 """
 
 import numpy as np
