@@ -718,6 +718,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   __shared__ int s_b;
   __shared__ int64_t s_above;
   __shared__ unsigned s_last, s_gen;
+  __shared__ unsigned long long s_pre;  // a chunk claimed ahead of the next refill
 #ifdef OTF_CUT_TRACE
   unsigned long long ts[7] = {0, 0, 0, 0, 0, 0, 0};
   CUT_STAMP(0);
@@ -731,13 +732,24 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   const int64_t nchunks = (n + kCutChunkRows - 1) / kCutChunkRows;  // >= 4 G (pq_cut_plan)
   const int64_t c0 = (int64_t)vb * nchunks / G;
   const int64_t rb = c0 * kCutChunkRows, re = n;
-  auto next_chunk = [&]() -> int64_t {  // the next dynamically assigned chunk, or -1
-    for (;;) {
-      const int64_t c = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(ws.cut_word + 8), 1ull);
-      if (c >= nchunks) return -1;
-      const int64_t b = (c * G + nchunks - 1) / nchunks;  // the only CTA whose c0 could be c
-      if (b >= (int64_t)G || b * nchunks / G != c) return c;
-    }
+  unsigned long long* chunk_ctr = reinterpret_cast<unsigned long long*>(ws.cut_word + 8);
+  auto is_first = [&](int64_t c) {  // chunk c is some CTA's first chunk c0
+    const int64_t b = (c * G + nchunks - 1) / nchunks;  // the only CTA whose c0 could be c
+    return b < (int64_t)G && b * nchunks / G == c;
+  };
+  // the next dynamically assigned chunk, or -1. A refill takes the claim made at the previous
+  // refill (s_pre) and requests the following one, so the TMA of the chunk is issued without
+  // waiting on the atomic's round trip (only the rare skipped first chunks of other CTAs do)
+  auto next_chunk = [&]() -> int64_t {
+    int64_t c = (int64_t)s_pre;
+    while (c < nchunks && is_first(c)) c = (int64_t)atomicAdd(chunk_ctr, 1ull);
+    return c < nchunks ? c : -1;
+  };
+  // (refills are serialised by the ring: the next one needs this warp's count on the other stage,
+  // which it adds after this store; the fence orders the two for the warp that reads s_pre)
+  auto pre_claim = [&]() {
+    s_pre = atomicAdd(chunk_ctr, 1ull);
+    __threadfence_block();
   };
   const uint32_t lut_bytes = (uint32_t)(16 * K * 8);
   if (threadIdx.x == 0) {
@@ -752,11 +764,13 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     // stream in while it finishes
     cut_issue(codes, re, rb, stage, &sbar, kCutBatchRows);
     stage_chunk[0] = c0;
+    pre_claim();
     for (int st = 1; st < kCutStages; ++st) {
       const int64_t c = next_chunk();
       stage_chunk[st] = c;
       if (c >= 0) cut_issue(codes, re, c * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
       else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
+      pre_claim();
     }
     s_tkey = 0u;
   }
@@ -973,6 +987,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       stage_chunk[st] = nc;  // published to the consumers by the barrier phase below
       if (nc >= 0) cut_issue(codes, re, nc * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
       else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
+      if (nc >= 0) pre_claim();  // (its round trip overlaps this warp's next batches)
     }
   }
   CUT_STAMP(4);
