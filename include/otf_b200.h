@@ -61,6 +61,10 @@ extern "C" {
 const char* otf_last_error(void);
 int otf_abi_version(void);
 int otf_device_count(int* out);
+/* Leave n SMs of `device` to other work (a concurrent trainer): the persistent rank kernels
+ * (fused dense / PQ selections) size their grids for the remaining SMs. 0 (default) = all.
+ * No reference counterpart (the reference trains and ranks on the host). */
+int otf_set_reserved_sms(int device, int32_t n);
 /* Names of the kernels this build contains, ';'-separated (for launch accounting). */
 const char* otf_kernel_names(void);
 /* Number of kernel launches issued by this process since load (all devices). */

@@ -54,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "otf_last_error": [],
     "otf_abi_version": [],
     "otf_device_count": [_P(_int)],
+    "otf_set_reserved_sms": [_int, _i32],
     "otf_kernel_names": [],
     "otf_launch_count": [],
     "otf_repo_create_dense": [_int, _vp, _i64, _i32, _vp, _i64, _int, _int, _P(_vp)],
@@ -165,6 +166,12 @@ def tptr(t) -> C.c_void_p:
 
 
 _device = None
+
+
+def set_reserved_sms(n: int, device: int | None = None) -> None:
+    """Leave ``n`` SMs to a concurrent trainer: the persistent rank kernels size their grids for
+    the rest (otf_set_reserved_sms). 0 restores the whole GPU."""
+    check(load().otf_set_reserved_sms(default_device() if device is None else device, int(n)))
 
 
 def default_device() -> int:

@@ -43,6 +43,15 @@ int sm_count(int device) {
 }
 
 
+// SMs the persistent rank kernels may use: all but `reserved` (otf_set_reserved_sms), so a
+// concurrent trainer's CTA always finds a free SM
+static std::atomic<int> g_reserved[64];
+int rank_sms(int device) {
+  const int n = sm_count(device) - g_reserved[device & 63].load(std::memory_order_relaxed);
+  return n > 1 ? n : 1;
+}
+int reserved_sms(int device) { return g_reserved[device & 63].load(std::memory_order_relaxed); }
+
 // Simple device/pinned buffers ---------------------------------------------------------------
 struct DevBuf {
   void* p = nullptr;
@@ -121,6 +130,7 @@ struct otf_repo {
     const void* key[16] = {};
     int64_t k = -1;
     int kernels = 0;  // kernels in the graph (launch accounting of each replay)
+    int reserved = 0;  // reserved SMs when captured (grid sizes depend on it)
     uint64_t used = 0;
   };
   std::vector<GraphEntry> graphs;  // <= kGraphCache entries, least recently used replaced
@@ -379,6 +389,12 @@ const char* otf_kernel_names(void) {
          "bin_hamming;split_w_half_kernel;absmax_kernel;topk_coop_kernel;pegasos_kernel;batch_train_kernel;hinge_objective_kernel;"
          "split_w_kernel;multi_score_tc;gather_rows_kernel;gather_i64_kernel;group_finalize_local;pq_rank_cut_kernel;dense_rank_cut;"
          "km_sqnorms;km_assign;km_objective;km_means;pq_cent_norms_kernel;pq_block_bounds_kernel;pq_encode_kernel";
+}
+
+int otf_set_reserved_sms(int device, int32_t n) {
+  if (n < 0 || n >= sm_count(device)) return fail(OTF_ERR_CONFIG, "reserved SMs must be in [0, SM count)");
+  g_reserved[device & 63].store(n, std::memory_order_relaxed);
+  return OTF_OK;
 }
 
 int otf_device_count(int* out) {
@@ -812,7 +828,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
                          h_in, h_out};
   otf_repo::GraphEntry* hit = nullptr;
   for (auto& ge : r->graphs) {
-    bool same = ge.exec && ge.k == k_eff;
+    bool same = ge.exec && ge.k == k_eff && ge.reserved == reserved_sms(r->device);
     for (int i = 0; i < 16 && same; ++i) same = ge.key[i] == key[i];
     if (same) { hit = &ge; break; }
   }
@@ -852,6 +868,7 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     for (int i = 0; i < 16; ++i) hit->key[i] = key[i];
     hit->k = k_eff;
     hit->kernels = kernels;
+    hit->reserved = reserved_sms(r->device);
   }
   hit->used = ++r->graph_clock;
   OTF_CUDA(cudaGraphLaunch(hit->exec, st));

@@ -553,7 +553,7 @@ int dc_grid(int device) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kDcThreads, kDcSmem) != cudaSuccess) return 0;
     per_sm[device & 63] = b;
   }
-  return per_sm[device & 63] * sm_count(device);
+  return per_sm[device & 63] * rank_sms(device);
 }
 
 int dc_grid_of(int cpl, int device) {

@@ -31,6 +31,10 @@ struct NvtxRange {
 };
 #define OTF_NVTX(name) ::otf::NvtxRange _otf_nvtx_range(name)
 
+// SMs the persistent rank kernels size their grids for (all but the reserved ones)
+int rank_sms(int device);
+int reserved_sms(int device);
+
 // a handle created over a borrowed device payload takes ownership of it (file loaders)
 void repo_own_payload(otf_repo* r);
 

@@ -1063,7 +1063,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
 bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int device, int* r) {
   static const bool off = getenv("OTF_PQ_NO_CUT") != nullptr;  // A/B switch (tools/)
   if (off || M != 16 || !pq_fast_path(M, codes) || k_eff <= 0) return false;
-  const int g = std::min(sm_count(device), kCutSampleCtasMax);
+  const int g = std::min(rank_sms(device), kCutSampleCtasMax);
   if (n < (int64_t)g * kCutChunkRows * 4) return false;  // >= 4 chunks per CTA
   if (2 * g > kCutScanThreads) return false;              // one sample maximum per selecting thread
   const int64_t S = (int64_t)g * kCutBatchRows;            // batch 0 of every CTA's first chunk
@@ -1091,7 +1091,7 @@ int launch_pq_rank_cut(const float* cents, int K, int Q, const double* w, double
     OTF_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRcSmem));
     configured[device & 63] = true;
   }
-  const int g = std::min(sm_count(device), kCutSampleCtasMax);
+  const int g = std::min(rank_sms(device), kCutSampleCtasMax);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(kCutScanThreads);
