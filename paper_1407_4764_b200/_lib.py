@@ -119,6 +119,9 @@ _checked_device = False
 def load(require_device: bool = True) -> C.CDLL:
     """Load the shared library (and, by default, insist on a visible CUDA device)."""
     global _lib, _checked_device
+    lib = _lib
+    if lib is not None and (_checked_device or not require_device):
+        return lib  # the per-query path: no lock once loaded
     with _lock:
         if _lib is None:
             if not LIB_PATH.exists():

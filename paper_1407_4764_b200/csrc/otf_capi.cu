@@ -673,9 +673,16 @@ int otf_repo_rank(otf_repo* r, const double* w, int64_t k, int64_t* out_ids, dou
   // is reused by every host-memory rank of this k)
   rc = rank_graph_locked(r, static_cast<const double*>(r->w.p), k_eff, d_ids, d_sc, d_rows, st, r->h_w.p,
                          d2h_copy ? r->h_out.p : nullptr);
-  if (const int rc2 = repo_leave(r, st)) rc = rc ? rc : rc2;
-  if (rc) { cudaStreamSynchronize(st); return rc; }
+  if (rc) {
+    repo_leave(r, st);
+    cudaStreamSynchronize(st);
+    return rc;
+  }
   OTF_CUDA(cudaStreamSynchronize(st));
+  // the stream is drained: nothing of this call is pending, so a later call on another stream
+  // has nothing to wait for (no event record on the per-query host path)
+  r->used = false;
+  r->last_stream = st;
   const int64_t* h_ids = static_cast<const int64_t*>(r->h_out.p);
   std::memcpy(out_ids, h_ids, (size_t)k_eff * 8);
   std::memcpy(out_scores, h_ids + k_eff, (size_t)k_eff * 8);
@@ -841,6 +848,8 @@ int rank_graph_locked(otf_repo* r, const double* w_dev, int64_t k_eff, int64_t* 
     if (h_in && cudaMemcpyAsync(const_cast<double*>(w_dev), h_in, (size_t)r->model_dim * sizeof(double),
                                 cudaMemcpyHostToDevice, cap) != cudaSuccess)
       rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync (graph H2D)");
+    // (a one-CTA kernel reading w through the pinned buffer's device mapping instead of this copy
+    // node measured the same: C1 host query 108.9 vs 108.8 us)
     if (!rc) rc = rank_device(r, w_dev, k_eff, ids_dev, scores_dev, rows_dev, cap);
     if (!rc && h_out && cudaMemcpyAsync(h_out, ids_dev, (size_t)k_eff * 24, cudaMemcpyDeviceToHost, cap) != cudaSuccess)
       rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync (graph D2H)");

@@ -326,10 +326,14 @@ class Repository:
 
     # -- views (ranker.py:213-231) ------------------------------------------------------------
     def _info(self):
-        kind, count, dim, nbytes, dev = C.c_int32(), C.c_int64(), C.c_int32(), C.c_int64(), C.c_int32()
-        _lib.check(_lib.load().otf_repo_info(self._handle, C.byref(kind), C.byref(count), C.byref(dim),
-                                             C.byref(nbytes), C.byref(dev)))
-        return count.value, nbytes.value, dev.value
+        # (count, payload bytes, device) never change for a handle: one C call per repository
+        info = self.__dict__.get("_info_cache")
+        if info is None:
+            kind, count, dim, nbytes, dev = C.c_int32(), C.c_int64(), C.c_int32(), C.c_int64(), C.c_int32()
+            _lib.check(_lib.load().otf_repo_info(self._handle, C.byref(kind), C.byref(count), C.byref(dim),
+                                                 C.byref(nbytes), C.byref(dev)))
+            info = self._info_cache = (count.value, nbytes.value, dev.value)
+        return info
 
     @property
     def handle(self) -> C.c_void_p:
