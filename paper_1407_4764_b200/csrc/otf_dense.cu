@@ -540,7 +540,10 @@ static int launch_fast(const float* X, int64_t n, const double* w, float* out, u
 
 // ---- fused rank launch ---------------------------------------------------------------------------
 namespace {
-int dc_R(int cpl) { return cpl == 1 ? 32 : cpl == 2 ? 4 : cpl == 4 ? 2 : cpl == 16 ? 2 : 1; }
+#ifndef OTF_DC_R1  // rows per warp iteration of the fused kernel at d = 128
+#define OTF_DC_R1 32
+#endif
+int dc_R(int cpl) { return cpl == 1 ? OTF_DC_R1 : cpl == 2 ? 4 : cpl == 4 ? 2 : cpl == 16 ? 2 : 1; }
 
 template <int CPL, int R>
 int dc_grid(int device) {
@@ -558,7 +561,7 @@ int dc_grid(int device) {
 
 int dc_grid_of(int cpl, int device) {
   switch (cpl) {
-    case 1: return dc_grid<1, 32>(device);
+    case 1: return dc_grid<1, OTF_DC_R1>(device);
     case 2: return dc_grid<2, 4>(device);
     case 4: return dc_grid<4, 2>(device);
     case 8: return dc_grid<8, 1>(device);
@@ -619,7 +622,7 @@ int launch_dense_rank_cut(const float* X, int64_t n, int32_t d, const double* w,
                           int64_t id_base, int64_t k_eff, const DenseCutPlan& pl, TopkWs* ws, float* scratch,
                           int64_t* out_ids, double* out_scores, int64_t* out_rows, cudaStream_t st) {
   switch (d / 128) {
-    case 1: return dc_launch<1, 32>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
+    case 1: return dc_launch<1, OTF_DC_R1>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
     case 2: return dc_launch<2, 4>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
     case 4: return dc_launch<4, 2>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);
     case 8: return dc_launch<8, 1>(X, n, w, ids, id_base, k_eff, pl, ws, scratch, out_ids, out_scores, out_rows, st);

@@ -11,12 +11,12 @@ timeout 900 python bench.py > gpurun_out/r2f_bench.log 2>&1; echo bench=$?; line
 for c in c1 c2 c3 c4 c5a c5b c3e c3k; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu > gpurun_out/r2f_$c.log 2>&1; line gpurun_out/r2f_$c.log $c
 done
-for c in c2 c4; do
+for c in c1 c2 c4; do
   OTF_DENSE_NO_CUT=1 timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu --no-train > gpurun_out/r2f_${c}_nocut.log 2>&1; line gpurun_out/r2f_${c}_nocut.log "$c-nocut"
   timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu --no-train > gpurun_out/r2f_${c}_cut.log 2>&1; line gpurun_out/r2f_${c}_cut.log "$c-cut"
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2f_ref.log 2>&1; echo ref=$?; tail -1 gpurun_out/r2f_ref.log | cut -c1-400
-for spec in "c1:dense_score|topk:2" "c2:dense_rank_cut:1" "c4:dense_rank_cut:1" "c3:pq_rank_cut|pq_build_lut:2" "c5a:bin_score|topk:3" "c5b:multi_score|topk_seg:2"; do
+for spec in "c1:dense_rank_cut:1" "c2:dense_rank_cut:1" "c4:dense_rank_cut:1" "c3:pq_rank_cut|pq_build_lut:2" "c5a:bin_score|topk:3" "c5b:multi_score|topk_seg:2"; do
   IFS=: read cfg kr cnt <<< "$spec"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2f_$cfg.csv \
       python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-train > /dev/null 2>&1; echo launches_$cfg=$?
