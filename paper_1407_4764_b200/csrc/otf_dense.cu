@@ -434,6 +434,9 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
     const int nw = blockDim.x >> 5;
     for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
       const uint32_t ki = sk[q];
+      // the candidate's record and row are in flight during the count (L2 round trips)
+      const ulonglong2 ci = __ldcg(cut_rec + q);
+      const int64_t ri = __ldcg(ws.cut_row + q);
       int cnt = 0;
       unsigned tie = 0;  // some lane saw another candidate with the same key
 #pragma unroll 8
@@ -443,8 +446,6 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
         tie |= kj == ki && j != q;
       }
       if (__any_sync(0xffffffffu, tie)) {  // exact key ties: (~id desc, row asc) decides
-        const ulonglong2 ci = __ldcg(cut_rec + q);
-        const int64_t ri = __ldcg(ws.cut_row + q);
         for (int j = lane; j < C; j += 32) {
           if (sk[j] != ki || j == q) continue;
           const uint64_t ij = __ldcg(&cut_rec[j].y);
@@ -454,10 +455,9 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       if (lane == 0 && cnt < k_eff) {
-        const ulonglong2 ci = __ldcg(cut_rec + q);
         out_ids[cnt] = id_of_inv(ci.y);
         out_scores[cnt] = (double)__uint_as_float((uint32_t)ci.x);
-        if (out_rows) out_rows[cnt] = __ldcg(ws.cut_row + q);
+        if (out_rows) out_rows[cnt] = ri;
       }
     }
 #ifdef OTF_DCUT_TRACE

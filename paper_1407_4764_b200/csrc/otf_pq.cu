@@ -1013,6 +1013,9 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     // rank candidates i == vb (mod G): one warp per candidate counts who beats it
     for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
       const uint32_t ki = sk[q];
+      // the candidate's record and row are in flight during the count (L2 round trips)
+      const ulonglong2 ci = __ldcg(cut_rec + q);
+      const int64_t ri = __ldcg(ws.cut_row + q);
       int cnt = 0;
       unsigned tie = 0;
 #pragma unroll 8
@@ -1021,9 +1024,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
         cnt += kj > ki;
         tie |= kj == ki && jj != q;
       }
-      const ulonglong2 ci = __ldcg(cut_rec + q);
       if (__any_sync(0xffffffffu, tie)) {  // equal prefixes: the full key, then ~id, then the row
-        const int64_t ri = __ldcg(ws.cut_row + q);
         for (int jj = lane; jj < C; jj += 32) {
           if (sk[jj] != ki || jj == q) continue;
           const ulonglong2 cj = __ldcg(cut_rec + jj);
@@ -1036,7 +1037,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       if (lane == 0 && cnt < k_eff) {
         out_ids[cnt] = id_of_inv(ci.y);
         out_scores[cnt] = key_to_f64(ci.x);
-        if (out_rows) out_rows[cnt] = __ldcg(ws.cut_row + q);
+        if (out_rows) out_rows[cnt] = ri;
       }
     }
 #ifdef OTF_CUT_TRACE
