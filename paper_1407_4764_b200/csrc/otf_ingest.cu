@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <climits>
 #include <cstdio>
 #include <chrono>
 #include <cstdlib>
@@ -118,8 +119,16 @@ int check_magic(const File& f, const char magic[4]) {
   return OTF_OK;
 }
 
+// rows x width bytes, or -1 when that does not fit in an int64 (a corrupt header: "truncated")
+int64_t payload_bytes(uint64_t rows, uint64_t width) {
+  if (width != 0 && rows > (uint64_t)INT64_MAX / width) return -1;
+  return (int64_t)(rows * width);
+}
+
 // the payload is the rest of the file: shorter -> truncated, longer -> trailing bytes
 int check_payload(const File& f, int64_t off, int64_t bytes, const char* what) {
+  if (bytes < 0)
+    return fail(OTF_ERR_CORRUPTION, std::string("truncated file: the header's ") + what + " does not fit in a file");
   const int64_t have = std::max<int64_t>(0, f.size - off);
   if (have < bytes)
     return fail(OTF_ERR_CORRUPTION, "truncated file: expected " + std::to_string(bytes) + " bytes of " + what +
@@ -257,7 +266,7 @@ int otf_repo_load_dense(int device, const char* path, int normalize, otf_repo** 
   if (rc) return rc;
   if (dim == 0 || count == 0)
     return fail(OTF_ERR_EMPTY, f.path + ": empty store (count=" + std::to_string(count) + ", dim=" + std::to_string(dim) + ")");
-  const int64_t bytes = (int64_t)count * dim * 4;
+  const int64_t bytes = payload_bytes(count, (uint64_t)dim * 4);
   if ((rc = check_payload(f, 20, bytes, "feature payload"))) return rc;
   float* x = nullptr;
   OTF_CUDA(cudaMalloc(&x, (size_t)bytes));
@@ -299,7 +308,7 @@ int otf_repo_load_pq(int device, const char* path, const float* centroids, int32
   if (!rc) rc = read_exact(f, 8, &count, 8, "count");
   if (!rc) rc = read_exact(f, 16, &blocks, 4, "num_blocks");
   if (rc) return rc;
-  const int64_t bytes = (int64_t)count * blocks;
+  const int64_t bytes = payload_bytes(count, blocks);
   if ((rc = check_payload(f, 20, bytes, "code payload"))) return rc;
   // Repository.quantized: the codes must have the codebook's block count (ranker.py:188-189)
   if ((int64_t)blocks != (int64_t)num_blocks)
@@ -338,7 +347,7 @@ int otf_repo_load_binary(int device, const char* path, int32_t code_bytes, const
   if (!rc) rc = read_exact(f, 16, &bits, 4, "output_bits");
   if (rc) return rc;
   const int row_bytes = (int)((bits + 7) / 8);
-  const int64_t bytes = (int64_t)count * row_bytes;
+  const int64_t bytes = payload_bytes(count, (uint64_t)row_bytes);
   if ((rc = check_payload(f, 20, bytes, "code payload"))) return rc;
   if (out_bits) *out_bits = (int32_t)bits;
   // Repository.binary: the codes must have the codec's row width (ranker.py:205-206)

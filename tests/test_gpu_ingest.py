@@ -84,6 +84,12 @@ def test_codes_errors(otf, tmp_path):
         otf.Repository.load_quantized(book, path, ids=np.arange(4))
     with pytest.raises(FileNotFoundError):
         otf.Repository.load_quantized(book, tmp_path / "missing.otfc")
+    path.write_bytes(head(b"OTFC", ("<Q", 1 << 62), ("<I", 2)) + bytes(8))  # a corrupt count
+    with pytest.raises(otf.CorruptionError, match="truncated"):
+        otf.Repository.load_quantized(book, path)
+    path.write_bytes(head(b"OTFC", ("<Q", (1 << 64) - 1), ("<I", 8)))  # rows x width overflows
+    with pytest.raises(otf.CorruptionError, match="truncated"):
+        otf.Repository.load_quantized(book, path)
 
 
 def test_binary_round_trip_and_errors(otf, tmp_path):
