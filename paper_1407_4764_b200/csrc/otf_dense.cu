@@ -206,7 +206,9 @@ constexpr size_t kDcSmem = (size_t)kDcSelCap * 4 > (size_t)kDcFallbackK * 16 ? (
                                                                               : (size_t)kDcFallbackK * 16;
 constexpr int kDcPub = 4;         // sample keys published per CTA
 constexpr int kDcPerThread = 8;   // published keys per thread in the T search (G <= 512)
-constexpr int kDcHold = 1;        // scan groups a warp scores while the grid synchronises
+#ifndef OTF_DC_HOLD_SMALL  // scan groups a warp scores while the grid synchronises (R <= 2)
+#define OTF_DC_HOLD_SMALL 1
+#endif
 #ifdef OTF_DCUT_TRACE  // diagnostic build: per-CTA globaltimer stamps of the phases
 #define DC_STAMP(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[i]))
 #else
@@ -292,6 +294,7 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
     return g;
   };
   int64_t gcur = next_group(warp);
+  constexpr int kDcHold = R <= 2 ? OTF_DC_HOLD_SMALL : 1;
   float held[kDcHold];
   int64_t heldg[kDcHold];
 #pragma unroll
