@@ -604,7 +604,14 @@ bool dense_cut_plan(int32_t d, const float* X, int64_t n, int64_t k_eff, int dev
   const int cpl = d / 128;
   if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && cpl != 16 && cpl != 32) return false;
   // ~2 k + 128 candidates are expected; their count must stay well inside the shared-memory cap
-  const int64_t want = 2 * k_eff + 128;
+#ifndef OTF_CUT_WANT16  // expected candidates = k (OTF_CUT_WANT16 / 16) + 128
+#define OTF_CUT_WANT16 25
+#endif
+  // ~k (1 + 4.5 / sqrt(64)) + 128 candidates expected: at r ~ 64 the count's relative spread is
+  // ~1/8, so fewer than k (the exact fallback) is ~3.5 sigma away; the rounding of T down to its
+  // 16-bit prefix adds margin. Measured: C3 62.5 (2 k + 128) -> 61.8 us, C1 / C2 unchanged;
+  // 1.25 k + 128 was faster on C3 (59.9 us) but only ~2 sigma from a fallback.
+  const int64_t want = k_eff * OTF_CUT_WANT16 / 16 + 128;
   if (2 * want > kDcSelCap || k_eff > kDcFallbackK) return false;
   const int grid = dc_grid_of(cpl, device);
   if (grid <= 0) return false;
