@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256, 2) dense_score_fast(const float* __restri
 //      and the CTA publishes its four largest sample keys; a split grid barrier: while the other
 //      CTAs finish their sample, each warp scores its first scan group and holds the scores in
 //      registers (HBM stays busy); every CTA then takes T = the r-th largest of the 4 G published
-//      keys at 16-bit key resolution (r ~ (2 k + 128) x sample / n, so ~2 k + 128 rows are
+//      keys at 16-bit key resolution (r ~ want x sample / n, want ~ 1.56 k + 128, so ~want rows are
 //      expected at or above T), rounded down to that key prefix's lower edge;
 //   2. the scan: warp w scores groups w, w + nwarp, ... (interleaved as dense_score_fast, the
 //      sample groups skipped) and appends (key, ~id, row) of every row with key >= T to a
@@ -603,7 +603,7 @@ bool dense_cut_plan(int32_t d, const float* X, int64_t n, int64_t k_eff, int dev
   if (off || k_eff <= 0 || d % 128 != 0 || (((uintptr_t)X) & 15) != 0) return false;
   const int cpl = d / 128;
   if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && cpl != 16 && cpl != 32) return false;
-  // ~2 k + 128 candidates are expected; their count must stay well inside the shared-memory cap
+  // ~want candidates are expected (below); their count must stay well inside the shared-memory cap
 #ifndef OTF_CUT_WANT16  // expected candidates = k (OTF_CUT_WANT16 / 16) + 128
 #define OTF_CUT_WANT16 25
 #endif

@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kScanF32Threads, 1) pq_scan16_f32bins(const ui
 //      grid barrier: while the other CTAs finish their sample, each CTA scores the next three
 //      batches of its ring (held: their screening scores stay in registers, their codes in the
 //      stages); then every CTA takes T = the r-th largest of the 2 G published keys at 16-bit key
-//      resolution (r ~ (2 k_eff + 128) x sample / n, so ~2 k_eff + 128 rows are expected at or
+//      resolution (r ~ want x sample / n, want ~ 1.56 k_eff + 128, so ~want rows are expected at or
 //      above T), rounded down to that prefix's lower edge;
 //   2. emits every row whose float32 screening score s32 can reach T (s32 >= T - eps, |s32 -
 //      s64| <= eps as in pq_scan16_f32bins) AND whose exact float64 score (numpy's order, from
@@ -1068,7 +1068,7 @@ bool pq_cut_plan(int M, const uint8_t* codes, int64_t n, int64_t k_eff, int devi
   if (n < (int64_t)g * kCutChunkRows * 4) return false;  // >= 4 chunks per CTA
   if (2 * g > kCutScanThreads) return false;              // one sample maximum per selecting thread
   const int64_t S = (int64_t)g * kCutBatchRows;            // batch 0 of every CTA's first chunk
-  // ~2 k_eff + 128 rows are expected at or above the r-th largest of the S sampled scores (the
+  // ~want rows are expected at or above the r-th largest of the S sampled scores (the
   // r-th order statistic of the sample: relative spread ~1/sqrt(r), so fewer than k_eff rows or
   // more than the kRcCand candidate slots of the selection are both many sigmas away); the CTAs
   // publish their top two, so r <= g / 2 keeps the estimate close to the true r-th sample
