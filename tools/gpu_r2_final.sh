@@ -8,7 +8,7 @@ print('$2', 'step_ms', round(d['ms_per_step'],4), 'value', '%.4g' % d['value'], 
 s=$(date +%s); timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/r2f_tests.log 2>&1; echo tests=$? $(( $(date +%s)-s ))s; tail -2 gpurun_out/r2f_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
 timeout 900 python bench.py > gpurun_out/r2f_bench.log 2>&1; echo bench=$?; line gpurun_out/r2f_bench.log default
-for c in c1 c2 c3 c4 c5a c5b c3e c3k; do
+for c in c1 c2 c3 c3x c4 c5a c5b c3e c3k; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu > gpurun_out/r2f_$c.log 2>&1; line gpurun_out/r2f_$c.log $c
 done
 for c in c1 c2 c4; do
