@@ -329,10 +329,108 @@ __global__ void __launch_bounds__(256) pq_scan16_xor(const uint8_t* __restrict__
   }
 }
 
+// ---- M == 16 score() path: float64 scores, one byte_perm per lookup (round 2) -------------------
+// pq_scan16_xor computes every lookup address with a shift and a mask (ncu: ALU pipe 64%, 142
+// warp instructions per 32 rows — issue-bound). Here the float64 entry (m, j) sits at byte
+// (j << 8) | (m << 3) of a 256-byte line per code value j (the rank path's line layout, float32
+// half unused), so the address of sub-code t ^ s is ONE byte_perm of the code word with a
+// per-lane constant, as in the float32 screening; lanes of a half-warp read 16 different m:
+// conflict-free. The XOR order of the terms keeps numpy's pairwise sum bit-identical
+// (pq_scan16_xor's argument).
+constexpr int kScore16Threads = 512;  // 2 CTAs x 16 warps per SM (64 KB of lines each)
+constexpr size_t kScore16Smem = 256 * 256;
+
+template <int ROWS>
+__global__ void __launch_bounds__(kScore16Threads, 2) pq_score16_lines(const uint8_t* __restrict__ codes, int64_t n,
+                                                                  const double* __restrict__ lut_g, int K,
+                                                                  double* __restrict__ out) {
+  extern __shared__ __align__(1024) unsigned char sm[];  // 256 lines x 256 B (float64 half used)
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // (after the LUT kernel)
+  {
+    // all loads in flight before the first store (a load-store loop pays one L2 round trip per entry batch)
+    constexpr int kPer = 16 * 256 / kScore16Threads;
+    const int m = threadIdx.x & 15;  // 16 lanes fill one 128-byte run of a line
+    double v[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int j = (threadIdx.x + i * kScore16Threads) >> 4;
+      v[i] = j < K ? __ldg(lut_g + m * K + j) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      *reinterpret_cast<double*>(sm + (((threadIdx.x + i * kScore16Threads) >> 4) << 8) + (m << 3)) = v[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t s = lane & 15;
+  uint32_t kw[8];  // byte 0 / 1: (2u ^ s) << 3, (2u + 1 ^ s) << 3 — the entry offset inside a line
+#pragma unroll
+  for (int u = 0; u < 8; ++u) kw[u] = (((uint32_t)(2 * u) ^ s) << 3) | ((((uint32_t)(2 * u + 1) ^ s) << 3) << 8);
+  uint32_t sel[4];  // result byte 0 <- kw byte (t & 1), byte 1 <- code byte ((t ^ s) & 3), bytes 2, 3 <- 0
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sel[q] = 0x7604u | (uint32_t)(q & 1) | ((((uint32_t)q ^ s) & 3u) << 4);
+  const uint4* C4 = reinterpret_cast<const uint4*>(codes);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
+  uint4 nu[ROWS];
+  int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * ROWS;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int64_t row = base + 32 * i + lane;
+    nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+  }
+  for (; base < n; base += stride) {
+    uint4 u[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      u[i] = nu[i];
+      const int64_t row = base + stride + 32 * i + lane;
+      nu[i] = row < n ? ld_stream_u4(C4 + row) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const int64_t row = base + 32 * i + lane;
+      // words permuted by s & 8 (halves) and s & 4 (words): word t >> 2 holds sub-codes 4 (t >> 2) ^ s..
+      const uint32_t x0 = u[i].x, x1 = u[i].y, x2 = u[i].z, x3 = u[i].w;
+      const uint32_t t0 = sel_u32(s & 8, x2, x0), t1 = sel_u32(s & 8, x3, x1);
+      const uint32_t t2 = sel_u32(s & 8, x0, x2), t3 = sel_u32(s & 8, x1, x3);
+      const uint32_t wd[4] = {sel_u32(s & 4, t1, t0), sel_u32(s & 4, t0, t1), sel_u32(s & 4, t3, t2),
+                              sel_u32(s & 4, t2, t3)};
+      double b[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        b[t] = *reinterpret_cast<const double*>(sm + __byte_perm(wd[t >> 2], kw[t >> 1], sel[t & 3]));
+      double r[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) r[t] = __dadd_rn(b[t], b[t + 8]);
+      const double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      if (row < n) out[row] = res;
+    }
+  }
+}
+
 static int launch_scan16(const uint8_t* codes, int64_t n, const float* cents, const double* w,
                          const double* lut, int K, int Q, double* out, uint16_t* bins,
                          uint32_t* hist, int device, cudaStream_t st) {
   constexpr int ROWS = 4;
+  static const bool xor_kernel = getenv("OTF_PQ_SCORE_XOR") != nullptr;  // A/B switch (tools/)
+  if (lut && out && !bins && !hist && !xor_kernel) {
+    // the float64 score() path (round 2): one byte_perm per lookup
+    auto fs = pq_score16_lines<ROWS>;
+    static int per_sm_s[64] = {0};
+    if (!per_sm_s[device & 63]) {
+      OTF_CUDA(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScore16Smem));
+      int b = 0;
+      OTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fs, kScore16Threads, kScore16Smem));
+      per_sm_s[device & 63] = b > 0 ? b : 1;
+    }
+    int64_t grid = (int64_t)per_sm_s[device & 63] * sm_count(device);
+    const int64_t need = (n + kScore16Threads * ROWS - 1) / (kScore16Threads * ROWS);
+    if (need < grid) grid = need;
+    fs<<<(int)grid, kScore16Threads, kScore16Smem, st>>>(codes, n, lut, K, out);
+    OTF_LAUNCH_CHECK("pq_score16_lines");
+    return OTF_OK;
+  }
   auto fn = pq_scan16_xor<ROWS>;  // 48 KB static shared memory (LUT + histogram)
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
