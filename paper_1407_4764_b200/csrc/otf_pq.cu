@@ -717,10 +717,31 @@ __device__ __noinline__ void cut_emit(const unsigned char* sm, uint4 u0, uint4 u
 // codes do not depend on the LUT kernel). Warp w scores rows [256 w, 256 w + 256) of a chunk in
 // two batches of 4 rows per lane (one conflict-free 16-byte shared load per row); the last warp
 // done with a stage refills it with the CTA's chunk kCutStages ahead.
-constexpr int kCutScanThreads = 512;  // 16 warps x 4 rows per lane (1024 x 2 and 1024 x 1 measured slower)
+#ifndef OTF_CUT_THREADS
+#define OTF_CUT_THREADS 512
+#endif
+#ifndef OTF_CUT_STAGES
+#define OTF_CUT_STAGES 2
+#endif
+#ifndef OTF_CUT_BATCHES
+#define OTF_CUT_BATCHES 2
+#endif
+// Ring plans: 2 stages x 2 batches (64 KB chunks: one in flight while one is scored; the
+// default), or S >= 4 stages x 1 batch (32 KB chunks: up to S - 1 in flight). Measured (round 2,
+// -DOTF_CUT_NOCOMPUTE: the codes stream through the ring unscored): the 2 x 64 KB ring alone moves
+// C3x's 1.6 GB at 7.6 TB/s, so the scan is bound by the scoring (~55 warp instructions per row,
+// 16 warps per SM, latency-bound at ~40% issue), not the ring; 4 x 32 KB was 0.393 vs 0.317 ms
+// on C3x with scoring (code generation), 12 warps x 3 x 48 KB 0.404.
+constexpr int kCutScanThreads = OTF_CUT_THREADS;  // x 4 rows per lane (1024 x 2 and 1024 x 1 measured slower)
 constexpr int kCutRows = 4;           // rows per lane per batch
-constexpr int kCutBatches = 2;        // batches per warp per chunk
-constexpr int kCutStages = 2;
+constexpr int kCutBatches = OTF_CUT_BATCHES;  // batches per warp per chunk
+constexpr int kCutStages = OTF_CUT_STAGES;
+static_assert((kCutBatches == 2 && kCutStages == 2) || (kCutBatches == 1 && kCutStages >= 4), "ring plan");
+// the sample and the held batches: chunk c0's batches then the prologue's chunks (stage, batch)
+constexpr int kCutHeld = kCutBatches == 2 ? 3 : kCutStages - 2;  // batches scored while T is found
+constexpr int kCutHeldStages = kCutBatches == 2 ? 2 : kCutStages - 1;  // stages consumed before the main loop
+__host__ __device__ constexpr int cut_held_stage(int hb) { return kCutBatches == 2 ? (hb == 0 ? 0 : 1) : hb + 1; }
+__host__ __device__ constexpr int cut_held_batch(int hb) { return kCutBatches == 2 ? (hb == 0 ? 1 : hb - 1) : 0; }
 constexpr int kCutBatchRows = kCutScanThreads * kCutRows;      // 2048 (the sample: batch 0 of chunk 0)
 constexpr int kCutChunkRows = kCutBatchRows * kCutBatches;      // 4096
 constexpr int kCutChunkBytes = kCutChunkRows * 16;
@@ -788,7 +809,13 @@ __device__ __forceinline__ void cut_scores(const unsigned char* sm, const uint4 
   }
 }
 
-constexpr size_t kRcSmem = 256 * 256 + (size_t)kCutStages * kCutChunkBytes;  // 192 KB
+constexpr size_t kRcSmem = 256 * 256 + (size_t)kCutStages * kCutChunkBytes;  // 208 KB
+// the raw (M, K) LUT replica lands in the last stage (filled only after the rearrangement) when
+// there are three or more stages, else in the second half of stage 0
+constexpr bool kCutLutInLast = kCutStages > kCutHeldStages;
+constexpr size_t kCutLutOff = kCutLutInLast ? (size_t)(kCutStages - 1) * kCutChunkBytes : (size_t)kCutBatchRows * 16;
+static_assert(kCutLutOff + 16 * 256 * 8 <= (size_t)kCutStages * kCutChunkBytes, "LUT replica fits its stage");
+static_assert(kCutLutInLast || kCutBatches == 2, "stage plan");
 constexpr int kRcCand = 8192;  // candidates the selection ranks in shared memory (32-bit key prefixes)
 static_assert((size_t)kRcCand * 4 <= kRcSmem, "selection reuses the scan's shared memory");
 
@@ -816,7 +843,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   __shared__ int s_b;
   __shared__ int64_t s_above;
   __shared__ unsigned s_last, s_gen;
-  __shared__ unsigned long long s_pre;  // a chunk claimed ahead of the next refill
+  __shared__ unsigned long long s_pre;  // static round-robin rounds this CTA has taken
 #ifdef OTF_CUT_TRACE
   unsigned long long ts[7] = {0, 0, 0, 0, 0, 0, 0};
   CUT_STAMP(0);
@@ -831,26 +858,43 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   const int64_t c0 = (int64_t)vb * nchunks / G;
   const int64_t rb = c0 * kCutChunkRows, re = n;
   unsigned long long* chunk_ctr = reinterpret_cast<unsigned long long*>(ws.cut_word + 8);
+  const bool small32 = (uint64_t)nchunks * G < (1ull << 32);  // 32-bit divisions suffice (every real size)
   auto is_first = [&](int64_t c) {  // chunk c is some CTA's first chunk c0
-    const int64_t b = (c * G + nchunks - 1) / nchunks;  // the only CTA whose c0 could be c
+    if (small32) {
+      const uint32_t nc = (uint32_t)nchunks, cc = (uint32_t)c;
+      const uint32_t b = (cc * G + nc - 1u) / nc;  // the only CTA whose c0 could be c
+      return b < G && b * nc / G == cc;
+    }
+    const int64_t b = (c * G + nchunks - 1) / nchunks;
     return b < (int64_t)G && b * nchunks / G == c;
   };
-  // the next dynamically assigned chunk, or -1. A refill takes the claim made at the previous
-  // refill (s_pre) and requests the following one, so the TMA of the chunk is issued without
-  // waiting on the atomic's round trip (only the rare skipped first chunks of other CTAs do)
+  // chunks after each CTA's first: the first 7/8 (whole rounds of G) in static round robin —
+  // CTA b takes b, b + G, b + 2G, ... with no atomic — then the tail from a global counter, so
+  // CTAs that stream faster take more of it and all finish together. (A claim's atomic stalls
+  // the warp that refills a stage, and that warp is the stage's laggard: claiming every chunk
+  // cost C3x 0.333 vs 0.317 ms with 7/8 static (3/4: 0.320, 1/2: 0.324); all-static was 2 us
+  // slower on C3 from the imbalance.)
+#ifndef OTF_CUT_STAT16  // sixteenths of the chunks in static rounds
+#define OTF_CUT_STAT16 14
+#endif
+  const int64_t stat_rounds = nchunks * OTF_CUT_STAT16 / 16 / G;
   auto next_chunk = [&]() -> int64_t {
-    int64_t c = (int64_t)s_pre;
-    while (c < nchunks && is_first(c)) c = (int64_t)atomicAdd(chunk_ctr, 1ull);
-    return c < nchunks ? c : -1;
-  };
-  // (refills are serialised by the ring: the next one needs this warp's count on the other stage,
-  // which it adds after this store; the fence orders the two for the warp that reads s_pre)
-  auto pre_claim = [&]() {
-    s_pre = atomicAdd(chunk_ctr, 1ull);
-    __threadfence_block();
+    for (;;) {
+      int64_t c;
+      if ((int64_t)s_pre < stat_rounds) {
+        c = (int64_t)s_pre * G + vb;
+        s_pre = s_pre + 1ull;
+        __threadfence_block();  // (the next refill may be another warp's)
+      } else {
+        c = stat_rounds * G + (int64_t)atomicAdd(chunk_ctr, 1ull);
+      }
+      if (c >= nchunks) return -1;
+      if (!is_first(c)) return c;
+    }
   };
   const uint32_t lut_bytes = (uint32_t)(16 * K * 8);
   if (threadIdx.x == 0) {
+    s_pre = 0ull;  // static rounds taken
     for (int st = 0; st < kCutStages; ++st) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cut_smem_u32(&full[st])));
       done[st] = 0u;
@@ -860,15 +904,14 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the codes do not depend on the LUT kernel: the sample (batch 0 of chunk c0) and chunk 1
     // stream in while it finishes
-    cut_issue(codes, re, rb, stage, &sbar, kCutBatchRows);
+    cut_issue(codes, re, rb, stage, kCutBatches == 2 ? &sbar : &full[0], kCutBatchRows);
     stage_chunk[0] = c0;
-    pre_claim();
     for (int st = 1; st < kCutStages; ++st) {
       const int64_t c = next_chunk();
       stage_chunk[st] = c;
+      if (kCutLutInLast && st == kCutStages - 1) continue;  // the LUT lands there first
       if (c >= 0) cut_issue(codes, re, c * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
       else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
-      pre_claim();
     }
     s_tkey = 0u;
   }
@@ -882,7 +925,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cut_smem_u32(&lbar)), "r"(lut_bytes)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     cut_smem_u32(stage + kCutBatchRows * 16)),
+                     cut_smem_u32(stage + kCutLutOff)),
                  "l"(rep), "r"(lut_bytes), "r"(cut_smem_u32(&lbar))
                  : "memory");
   }
@@ -890,7 +933,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   {
     // 16 x 16 diagonal blocks per half-warp: lane l moves entry (m = l & 15, j = j0 + m) — the
     // raw reads (bank 2 j) and the line writes (bank 2 m) are both conflict-free
-    const double* raw = reinterpret_cast<const double*>(stage + kCutBatchRows * 16);
+    const double* raw = reinterpret_cast<const double*>(stage + kCutLutOff);
     const int m = lane & 15;
     uint32_t mx = 0u;
     for (int j0 = 2 * wid + (lane >> 4); j0 < 256; j0 += 2 * nw) {
@@ -906,9 +949,17 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
     if (lane < 16) atomicMax(&smx[m], mx);
   }
-  __syncthreads();  // every read of the raw LUT is done: chunk c0's second half may land there
-  if (threadIdx.x == 0)
-    cut_issue(codes, re, rb + kCutBatchRows, stage + kCutBatchRows * 16, &full[0], kCutChunkRows - kCutBatchRows);
+  __syncthreads();  // every read of the raw LUT is done: chunk c0's second half (or the last stage's chunk) may land there
+  if (threadIdx.x == 0) {
+    if (kCutBatches == 2)
+      cut_issue(codes, re, rb + kCutBatchRows, stage + kCutBatchRows * 16, &full[0], kCutChunkRows - kCutBatchRows);
+    if (kCutLutInLast) {
+      constexpr int st = kCutStages - 1;
+      const int64_t c = stage_chunk[st];
+      if (c >= 0) cut_issue(codes, re, c * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
+      else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
+    }
+  }
   // (pq_cut_plan keeps c0 + 1 <= nchunks - 1, so chunk c0 is full)
   float eps;
   bool screen;
@@ -941,7 +992,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   const int64_t row00 = rb + boff;
   {
     uint32_t ka = 0u, kb = 0u;  // this lane's two largest sample keys (0: below every key)
-    cut_wait(&sbar, 0u);
+    cut_wait(kCutBatches == 2 ? &sbar : &full[0], 0u);
     const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + boff;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) u0[i] = row00 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
@@ -963,31 +1014,26 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
     }
   }
   CUT_STAMP(1);
-  // split grid barrier: while the other CTAs finish their sample, score the three batches already
-  // in the ring (chunk c0's second half, the whole chunk in stage 1) and hold their scores
+  // split grid barrier: while the other CTAs finish their sample, score the batches already in
+  // the ring (kCutHeld: chunk c0's second batch and stage 1's chunk, or stages 1 .. S - 2) and
+  // hold their scores
   const unsigned gen = grid_arrive(ws.bar, G, &s_gen);
-  float hs[3][ROWS];
-  const int64_t c1 = stage_chunk[1];
-  {
-    cut_wait(&full[0], 0u);
-    const uint4* rows4 = reinterpret_cast<const uint4*>(stage) + kCutBatchRows + boff;
-    uint4 u[ROWS];
+  float hs[kCutHeld][ROWS];
 #pragma unroll
-    for (int i = 0; i < ROWS; ++i) u[i] = rows4[32 * i];
-    cut_scores<ROWS>(sm, u, kw, sel, s, hs[0]);
-    cut_wait(&full[1], 0u);
+  for (int hb = 0; hb < kCutHeld; ++hb) {
+    const int st = cut_held_stage(hb), bt = cut_held_batch(hb);
+    if (hb == 0 || st != cut_held_stage(hb - 1)) cut_wait(&full[st], 0u);
+    const int64_t c = stage_chunk[st];
+    if (c >= 0) {
+      const int64_t r0 = c * kCutChunkRows + bt * kCutBatchRows + boff;
+      const uint4* q4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + bt * kCutBatchRows + boff;
+      uint4 u[ROWS];
 #pragma unroll
-    for (int bt = 0; bt < 2; ++bt) {
-      if (c1 >= 0) {
-        const int64_t r0 = c1 * kCutChunkRows + bt * kCutBatchRows + boff;
-        const uint4* q4 = reinterpret_cast<const uint4*>(stage + kCutChunkBytes) + bt * kCutBatchRows + boff;
+      for (int i = 0; i < ROWS; ++i) u[i] = r0 + 32 * i < re ? q4[32 * i] : make_uint4(0, 0, 0, 0);
+      cut_scores<ROWS>(sm, u, kw, sel, s, hs[hb]);
+    } else {
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) u[i] = r0 + 32 * i < re ? q4[32 * i] : make_uint4(0, 0, 0, 0);
-        cut_scores<ROWS>(sm, u, kw, sel, s, hs[1 + bt]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < ROWS; ++i) hs[1 + bt][i] = -INFINITY;
-      }
+      for (int i = 0; i < ROWS; ++i) hs[hb][i] = -INFINITY;
     }
   }
   grid_wait(ws.bar, gen);
@@ -1036,11 +1082,10 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   if (usable) {
     if (__any_sync(0xffffffffu, max4(s0) >= t_emit)) emit_batch(u0, s0, row00);
 #pragma unroll 1
-    for (int hb = 0; hb < 3; ++hb) {  // (the held batches' codes are still in their stages)
+    for (int hb = 0; hb < kCutHeld; ++hb) {  // (the held batches' codes are still in their stages)
       if (!__any_sync(0xffffffffu, max4(hs[hb]) >= t_emit)) continue;
-      const int st = hb == 0 ? 0 : 1;
-      const int bt = hb == 0 ? 1 : hb - 1;
-      const int64_t r0 = (hb == 0 ? c0 : c1) * kCutChunkRows + bt * kCutBatchRows + boff;
+      const int st = cut_held_stage(hb), bt = cut_held_batch(hb);
+      const int64_t r0 = stage_chunk[st] * kCutChunkRows + bt * kCutBatchRows + boff;
       const uint4* q4 = reinterpret_cast<const uint4*>(stage + st * kCutChunkBytes) + bt * kCutBatchRows + boff;
       uint4 u[ROWS];
 #pragma unroll
@@ -1048,10 +1093,14 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       emit_batch(u, hs[hb], r0);
     }
   }
-  // both stages are consumed: the last warp done with each refills it
+#ifdef OTF_CUT_NOCOMPUTE
+  uint32_t nc_acc = 0u;
+#endif
+  // stages below kCutHeldStages are consumed: the last warp done with each refills it; a later
+  // stage s is first scored at j = s (its phase j / kCutStages, as for every later pass of every stage)
   for (int j = 0;; ++j) {
     const int st = j % kCutStages;
-    if (j >= kCutStages) {
+    if (j >= kCutHeldStages) {
       cut_wait(&full[st], (uint32_t)((j / kCutStages) & 1));
       const int64_t c = stage_chunk[st];
       if (c < 0) break;
@@ -1072,6 +1121,11 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
           for (int i = 0; i < ROWS; ++i) u[i] = row0 + 32 * i < re ? rows4[32 * i] : make_uint4(0, 0, 0, 0);
         }
         if (!usable) continue;
+#ifdef OTF_CUT_NOCOMPUTE  // (diagnostic) the ring alone: codes read from the stage, no scoring
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) nc_acc ^= u[i].x ^ u[i].y ^ u[i].z ^ u[i].w;
+        continue;
+#endif
         cut_scores<ROWS>(sm, u, kw, sel, s, sc);
         if (__any_sync(0xffffffffu, max4(sc) >= t_emit)) emit_batch(u, sc, row0);
       }
@@ -1085,12 +1139,20 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       stage_chunk[st] = nc;  // published to the consumers by the barrier phase below
       if (nc >= 0) cut_issue(codes, re, nc * kCutChunkRows, stage + st * kCutChunkBytes, &full[st]);
       else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cut_smem_u32(&full[st])) : "memory");
-      if (nc >= 0) pre_claim();  // (its round trip overlaps this warp's next batches)
     }
   }
   CUT_STAMP(4);
   grid_barrier(ws.bar, G);  // every candidate record is in place
   CUT_STAMP(5);
+#ifdef OTF_CUT_NOCOMPUTE
+  if (nc_acc == 0x9e3779b9u) ws.cut_word[3] += 1u;  // (keeps the reads)
+#ifdef OTF_CUT_TRACE
+  if (threadIdx.x == 0)
+    printf("cutT cta %d C 0 sample %.2f held %.2f threshold %.2f scan %.2f barrier %.2f select 0 total %.2f\n", (int)vb,
+           (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3,
+           (ts[5] - ts[4]) * 1e-3, (ts[5] - ts[0]) * 1e-3);
+#endif
+#endif
 
   // ---- 3. selection ----------------------------------------------------------------------------
   const unsigned long long c_all = __ldcg(cut_count);

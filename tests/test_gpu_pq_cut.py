@@ -80,8 +80,9 @@ def test_cut_fallback_threshold_too_high(otf, data):
     lut = O.build_score_lut(w, cents)
     best = np.argmax(lut, axis=1).astype(np.uint8)
     g = 148
-    nchunks = -(-N // 2048)
-    sampled = np.arange(g) * nchunks // g * 2048  # the first row of every sample CTA's chunk
+    chunk = 512 * 4 * 2  # kCutChunkRows (otf_pq.cu: kCutScanThreads x kCutRows x kCutBatches)
+    nchunks = -(-N // chunk)
+    sampled = np.arange(g) * nchunks // g * chunk  # the first row of every CTA's first chunk (its sample)
     codes[sampled] = best
     repo = otf.Repository.quantized(otf.PQCodebook(cents), codes)
     f0 = fallbacks(otf, repo)
