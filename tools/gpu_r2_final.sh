@@ -27,3 +27,5 @@ bash tools/gpu_cut_trace.sh > gpurun_out/r2f_cut_trace.txt 2>&1; tail -8 gpurun_
 CFG=c2 bash tools/gpu_dcut_trace.sh > gpurun_out/r2f_dcut_trace.txt 2>&1; tail -8 gpurun_out/r2f_dcut_trace.txt
 timeout 600 python tools/latency_probe.py c1 c3 c2 > gpurun_out/r2f_lat.log 2>&1; tail -12 gpurun_out/r2f_lat.log
 timeout 900 python tools/ingest_bench.py 100000000 /tmp > gpurun_out/r2f_ingest.log 2>&1; tail -4 gpurun_out/r2f_ingest.log
+timeout 300 python tools/pq_score_probe.py > gpurun_out/r2f_pq_score.log 2>&1; OTF_PQ_SCORE_XOR=1 timeout 300 python tools/pq_score_probe.py >> gpurun_out/r2f_pq_score.log 2>&1; cat gpurun_out/r2f_pq_score.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pq_score16 -s 3 -c 1 -o gpurun_out/prof_r2f_pq_score python tools/pq_score_probe.py > /dev/null 2>&1; echo full_pq_score=$?
