@@ -306,7 +306,7 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
       gcur = next_group(gcur + nwarp);
     }
   }
-  grid_wait(ws.bar, gen);
+  grid_wait(ws.bar, G, gen);
   DC_STAMP(2);
   // T = the r-th largest published key at 16-bit resolution (two 8-bit radix passes in shared
   // memory over the kDcPub G values, held in registers: one L2 round trip), rounded down to that

@@ -1036,7 +1036,7 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
       for (int i = 0; i < ROWS; ++i) hs[hb][i] = -INFINITY;
     }
   }
-  grid_wait(ws.bar, gen);
+  grid_wait(ws.bar, G, gen);
   CUT_STAMP(2);
   // T = the r-th largest of the 2 G sample maxima at 16-bit key resolution (two 8-bit radix
   // passes in shared memory), rounded down to that key's lower edge

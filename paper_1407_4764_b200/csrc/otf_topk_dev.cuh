@@ -14,48 +14,71 @@ static constexpr int kTopkCtasPerSm = 1;
 static constexpr int kCandCap = 8192;                       // candidates ranked in smem
 static constexpr size_t kTopkSmem = (size_t)kCandCap * 16;  // key + inv per candidate
 
-// Grid barrier on one 64-bit word {count (low half), generation (high half)}: an arrival is one
-// atomic; the last arrival starts the next generation and zeroes the count in ONE more atomic,
-// so waiters (polling the generation) are released one L2 round trip after the last arrival.
+// Grid barrier on one 64-bit word {count (low half), generation (high half)}. An arrival is one
+// atomic add of 1; the last arrival of a generation also adds (1 << 32) - nblocks (a reduction
+// nobody waits for) to keep the count small. The barrier a word state has completed is its
+// effective generation gen + count / nblocks, so waiters are released by the last ARRIVAL itself
+// (round 2: one L2 round trip sooner than waiting for the generation bump), and arrivals that
+// overtake a pending bump (count >= nblocks) count toward the next generation correctly.
+#ifndef OTF_BAR_GEN_ONLY
+__device__ __forceinline__ unsigned int bar_eff_gen(unsigned long long v, unsigned int nblocks) {
+  return (unsigned int)(v >> 32) + (unsigned int)v / nblocks;
+}
+// arrive: returns the effective generation this arrival belongs to (released once the word's
+// effective generation exceeds it)
+__device__ __forceinline__ unsigned int bar_arrive_t0(unsigned int* bar, unsigned int nblocks, bool* last = nullptr) {
+  unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
+  __threadfence();
+  const unsigned long long old = atomicAdd(word, 1ull);
+  const bool l = (unsigned int)old % nblocks == nblocks - 1;
+  if (l) atomicAdd(word, (1ull << 32) - nblocks);
+  if (last) *last = l;
+  return bar_eff_gen(old, nblocks);
+}
+__device__ __forceinline__ void bar_wait_t0(unsigned int* bar, unsigned int nblocks, unsigned int mine) {
+  volatile unsigned long long* vw = reinterpret_cast<volatile unsigned long long*>(bar);
+  while ((int)(bar_eff_gen(*vw, nblocks) - mine) <= 0) __nanosleep(20);  // (wrap-safe)
+  __threadfence();
+}
+#else  // (A/B) waiters poll the generation bump
+__device__ __forceinline__ unsigned int bar_arrive_t0(unsigned int* bar, unsigned int nblocks, bool* last = nullptr) {
+  unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
+  __threadfence();
+  const unsigned long long old = atomicAdd(word, 1ull);
+  const bool l = (unsigned int)old == nblocks - 1;
+  if (l) atomicAdd(word, (1ull << 32) - nblocks);
+  if (last) *last = l;
+  return (unsigned int)(old >> 32);
+}
+__device__ __forceinline__ void bar_wait_t0(unsigned int* bar, unsigned int, unsigned int gen) {
+  volatile unsigned int* vgen = bar + 1;
+  while (*vgen == gen) __nanosleep(20);
+  __threadfence();
+}
+#endif
+
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
-    __threadfence();
-    const unsigned long long old = atomicAdd(word, 1ull);
-    const unsigned int gen = (unsigned int)(old >> 32);
-    if ((unsigned int)old == nblocks - 1) {
-      atomicAdd(word, (1ull << 32) - nblocks);
-    } else {
-      volatile unsigned int* vgen = bar + 1;
-      while (*vgen == gen) __nanosleep(20);
-    }
-    __threadfence();
+    bool last;
+    const unsigned int mine = bar_arrive_t0(bar, nblocks, &last);
+    if (!last) bar_wait_t0(bar, nblocks, mine);  // (the last arrival has nothing to wait for)
+    else __threadfence();
   }
   __syncthreads();
 }
 
 // Split grid barrier (same word as grid_barrier): arrive, do independent work, then wait.
-// grid_arrive returns the generation to wait on (every thread of the CTA gets it).
+// grid_arrive returns the token to wait on (every thread of the CTA gets it).
 __device__ __forceinline__ unsigned int grid_arrive(unsigned int* bar, unsigned int nblocks, unsigned int* s_gen) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long* word = reinterpret_cast<unsigned long long*>(bar);
-    __threadfence();
-    const unsigned long long old = atomicAdd(word, 1ull);
-    *s_gen = (unsigned int)(old >> 32);
-    if ((unsigned int)old == nblocks - 1) atomicAdd(word, (1ull << 32) - nblocks);
-  }
+  if (threadIdx.x == 0) *s_gen = bar_arrive_t0(bar, nblocks);
   __syncthreads();
   return *s_gen;
 }
-__device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int gen) {
+__device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int nblocks, unsigned int token) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = bar + 1;
-    while (*vgen == gen) __nanosleep(20);
-    __threadfence();
-  }
+  if (threadIdx.x == 0) bar_wait_t0(bar, nblocks, token);
   __syncthreads();
 }
 
