@@ -33,9 +33,20 @@ namespace otf {
 // transposed float32 butterfly (32 rows per warp iteration, ~4 instructions per row). Slices
 // are chained through a float64 partial per row (8 B/row per extra slice, +3% traffic for
 // 2048-bit codes). Every row is summed in the same fixed order (position independent).
+//
+// WIDE (round 2, the default): the same lookups and the same sums, loaded 16 bytes at a time.
+// Lane l = 8 b + a reads bytes [16 a, 16 a + 16) of a slice of row 4 g + b (g = 0..7: one
+// LDG.128 per 4 rows instead of one LDG.32 per row), i.e. the words of "virtual lanes"
+// v = 4 a + q, q = 0..3. At step j it looks up word q = (j + b) & 3 (the 32 lanes then read 32
+// distinct virtual lanes = 32 banks: conflict-free). The transposed float32 reduction runs over
+// the 8 lanes of a row (xor 4, 2, 1 = virtual-lane bits 4, 3, 2) and ends with
+// (S0 + S2) + (S1 + S3) in-lane (bits 1, 0): the xor tree of the 32 virtual lanes, so every row's
+// score is the same bits as the narrow kernel's. LSU instructions per 32 rows and lane:
+// 8 + 128 + 28 (+2) instead of 32 + 128 + 31 (+2).
 constexpr int kBinThreads = 512;
+__device__ __forceinline__ uint32_t bin_sel(int c, uint32_t a, uint32_t b) { return c ? a : b; }
 
-template <int RB>  // row bytes (compile-time so per-row offsets are immediates)
+template <int RB, bool WIDE = true>  // row bytes (compile-time so per-row offsets are immediates)
 __global__ void __launch_bounds__(kBinThreads, 1)
 bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
                 const double* __restrict__ w, int n_bits, const double* __restrict__ partial_in,
@@ -61,8 +72,78 @@ bin_score_bytes(const uint8_t* __restrict__ codes, int64_t n, int slice,
   const uint32_t L = ((uint32_t)lane << 2) | (((uint32_t)lane << 2 | 0x80u) << 8) | (1u << 24);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint8_t* base = codes + (int64_t)slice * 128 + 4 * lane;
   constexpr int R = 32;  // rows per warp iteration
+  if (WIDE) {
+    const int a = lane & 7, b = lane >> 3;
+    uint32_t Lj[4];  // per-step constants: virtual lane 4 a + ((j + b) & 3)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t lv = 4u * a + ((j + b) & 3);
+      Lj[j] = (lv << 2) | ((lv << 2 | 0x80u) << 8) | (1u << 24);
+    }
+    const uint8_t* base16 = codes + (int64_t)slice * 128 + 16 * a;
+    const int slot = 4 * a + b;  // the row this lane finishes (transposed over g: g = a)
+    for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
+      if (use_pf && lane == 0) {
+        const int64_t nr = r0 + use_pf * nwarp * R;
+        if (nr < n)
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map), "r"(slice * 128),
+                       "r"((int)nr)
+                       : "memory");
+      }
+      uint4 u[8];
+      const uint8_t* rp = base16 + (r0 + b) * RB;
+      if (r0 + R <= n) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g) u[g] = __ldcs(reinterpret_cast<const uint4*>(rp + 4 * g * RB));
+      } else {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          u[g] = r0 + 4 * g + b < n ? __ldcs(reinterpret_cast<const uint4*>(rp + 4 * g * RB)) : make_uint4(0, 0, 0, 0);
+      }
+      const int64_t row = r0 + slot;
+      const bool active = row < n;
+      const double pin = active && partial_in ? __ldcs(partial_in + row) : 0.0;
+      float p[R];  // p[4 g + j]
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        // word (j + b) & 3 at step j: rotate the four words by b
+        const uint32_t t0 = bin_sel(b & 1, u[g].y, u[g].x), t1 = bin_sel(b & 1, u[g].z, u[g].y);
+        const uint32_t t2 = bin_sel(b & 1, u[g].w, u[g].z), t3 = bin_sel(b & 1, u[g].x, u[g].w);
+        const uint32_t r[4] = {bin_sel(b & 2, t2, t0), bin_sel(b & 2, t3, t1), bin_sel(b & 2, t0, t2),
+                               bin_sel(b & 2, t1, t3)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t x = r[j], L = Lj[j];
+          float s = *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6604));
+          s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6615)));
+          s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6724)));
+          s = __fadd_rn(s, *reinterpret_cast<const float*>(tabb + __byte_perm(x, L, 0x6735)));
+          p[4 * g + j] = s;
+        }
+      }
+      transposed_reduce_f<R, 8>(p, lane);  // -> p[0..3]: row group g = a, steps j = 0..3
+      double total = (double)__fadd_rn(__fadd_rn(p[0], p[2]), __fadd_rn(p[1], p[3]));
+      if (active && partial_in) total = __dadd_rn(pin, total);
+      if (out) {
+        const float sc = __double2float_rn(total);
+        if (active) out[row] = sc;
+        if (ghist) hist_add(sh, active, hist_bin(sc));
+        if (cmax) {
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, active ? hist_bin(sc) : 0u);
+          if (lane == 0) cmax[r0 / R] = (uint16_t)wm;
+        }
+      } else if (active) {
+        partial_out[row] = total;
+      }
+    }
+    if (ghist && out) {
+      __syncthreads();
+      hist_flush(sh, ghist);
+    }
+    return;
+  }
+  const uint8_t* base = codes + (int64_t)slice * 128 + 4 * lane;
   bool writer;
   const int slot = row_of_lane<R, 32>(lane, &writer);  // the row this lane finishes
   for (int64_t r0 = warp * R; r0 < n; r0 += nwarp * R) {
@@ -386,10 +467,10 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
     const size_t smem = (size_t)4 * 256 * 32 * sizeof(float);
     static bool configured[64] = {false};
     if (!configured[device & 63]) {
-      cudaFuncSetAttribute((const void*)bin_score_bytes<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute((const void*)bin_score_bytes<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute((const void*)bin_score_bytes<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute((const void*)bin_score_bytes<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)bin_score_bytes<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured[device & 63] = true;
     }
     // tensor map over the codes (u8, RB x n) for the in-kernel L2 prefetch of the next tile
@@ -458,6 +539,17 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       if (cmax && clog) *clog = 5;
       return OTF_OK;
     }
+    static const bool narrow = getenv("OTF_BIN_NARROW") != nullptr;  // A/B switch (tools/)
+    if (!narrow) {
+      static bool wconf[64] = {false};
+      if (!wconf[device & 63]) {
+        cudaFuncSetAttribute((const void*)bin_score_bytes<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute((const void*)bin_score_bytes<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute((const void*)bin_score_bytes<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute((const void*)bin_score_bytes<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        wconf[device & 63] = true;
+      }
+    }
     int64_t grid = sm_count(device);  // one 512-thread CTA per SM (128 KB table)
     const int64_t need = (n + (kBinThreads / 32) * 32 - 1) / ((kBinThreads / 32) * 32);
     if (need < grid) grid = need;
@@ -467,10 +559,22 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       double* pout = last ? nullptr : scratch;
       float* o = last ? out : nullptr;
       switch (row_bytes) {
-        case 128: bin_score_bytes<128><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
-        case 256: bin_score_bytes<256><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
-        case 512: bin_score_bytes<512><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
-        default: bin_score_bytes<1024><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr); break;
+        case 128:
+          if (narrow) bin_score_bytes<128, false><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          else bin_score_bytes<128, true><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          break;
+        case 256:
+          if (narrow) bin_score_bytes<256, false><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          else bin_score_bytes<256, true><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          break;
+        case 512:
+          if (narrow) bin_score_bytes<512, false><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          else bin_score_bytes<512, true><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          break;
+        default:
+          if (narrow) bin_score_bytes<1024, false><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          else bin_score_bytes<1024, true><<<(int)grid, kBinThreads, smem, st>>>(codes, n, s, w, n_bits, pin, pout, o, hist, map, use_pf, last ? cmax : nullptr);
+          break;
       }
       OTF_LAUNCH_CHECK("bin_score_bytes");
     }
