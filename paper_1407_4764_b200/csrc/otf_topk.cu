@@ -605,11 +605,24 @@ topk_seg_cut_kernel(const float* __restrict__ scores, int n_seg, int64_t n, cons
       for (int h = 0; h < kRuns; ++h)
         x[h] = ld_stream_f4(reinterpret_cast<const float4*>(scores + f0 + 128 * h + 4 * lane));
       const uint32_t t = s_T[sg0] ? s_T[sg0] : 0xffffffffu;
+      if (t > 0x80000000u) {
+        // T above +0.0 (the usual case): a key >= T needs a positive float whose bits, as a signed
+        // integer, are >= T ^ 0x80000000; negative floats (and -0.0) are negative integers, and a
+        // positive NaN passes to the exact test. One integer max per four scores.
+        const int tb = (int)(t ^ 0x80000000u);
 #pragma unroll
-      for (int h = 0; h < kRuns; ++h) {
-        const uint32_t kmax = max(max((uint32_t)score_key(x[h].x), (uint32_t)score_key(x[h].y)),
-                                  max((uint32_t)score_key(x[h].z), (uint32_t)score_key(x[h].w)));
-        if (kmax >= t) test4(f0 + 128 * h + 4 * lane, x[h], 4);
+        for (int h = 0; h < kRuns; ++h) {
+          const int m = max(max(__float_as_int(x[h].x), __float_as_int(x[h].y)),
+                            max(__float_as_int(x[h].z), __float_as_int(x[h].w)));
+          if (m >= tb) test4(f0 + 128 * h + 4 * lane, x[h], 4);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < kRuns; ++h) {
+          const uint32_t kmax = max(max((uint32_t)score_key(x[h].x), (uint32_t)score_key(x[h].y)),
+                                    max((uint32_t)score_key(x[h].z), (uint32_t)score_key(x[h].w)));
+          if (kmax >= t) test4(f0 + 128 * h + 4 * lane, x[h], 4);
+        }
       }
       continue;
     }
