@@ -670,8 +670,8 @@ topk_seg_cut_kernel(const float* __restrict__ scores, int n_seg, int64_t n, cons
   const unsigned C = __ldcg(w.count);
   DirectSrc<float> src{scores + (int64_t)sg * n};
   if (s_T[sg] != 0u && (int64_t)C >= k_eff && C <= (unsigned)kCandCap) {
-    rank_emit(src, w, (int64_t)C, k_eff, dyn, out_ids + (int64_t)sg * k_eff, out_scores + (int64_t)sg * k_eff, nullptr,
-              vb, per);
+    rank_emit_k32(src, w, (int64_t)C, k_eff, dyn, out_ids + (int64_t)sg * k_eff, out_scores + (int64_t)sg * k_eff,
+                  nullptr, vb, per);
     grid_barrier(w.bar, per);  // (the other path's kernels expect a zero count)
     if (vb == 0 && threadIdx.x == 0) *w.count = 0u;
     return;

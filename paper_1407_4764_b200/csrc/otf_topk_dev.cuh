@@ -363,6 +363,51 @@ __device__ void rank_emit(const Src& src, const TopkWs& ws, int64_t m, int64_t k
   }
 }
 
+// rank_emit for candidates whose keys fit in 32 bits (float32 scores): the count runs over 4-byte
+// keys in shared memory (one wavefront per 32 comparisons instead of four for the 16-byte
+// (key, inv) pairs); exact key ties — rare — are resolved by (~id desc, row asc) from global
+// memory, so equal (key, id) pairs still get distinct ranks. Round 2 (topk_seg_cut_kernel: the
+// 64 x ~2.1k-candidate rankings took ~285 us of its 0.74 ms with rank_emit).
+template <typename Src>
+__device__ void rank_emit_k32(const Src& src, const TopkWs& ws, int64_t m, int64_t k_eff, unsigned char* dyn,
+                              int64_t* out_ids, double* out_scores, int64_t* out_rows, unsigned vb, unsigned vnb) {
+  const int64_t mine = m > vb ? (m - 1 - vb) / vnb + 1 : 0;
+  if (mine == 0) return;
+  uint32_t* sk = reinterpret_cast<uint32_t*>(dyn);
+  for (int64_t t = threadIdx.x; t < m; t += blockDim.x) sk[t] = (uint32_t)__ldcg(ws.key + t);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mm = (int)m;  // m <= kCandCap
+  for (int64_t q = wid; q < mine; q += nw) {
+    const int i = (int)(vb + q * vnb);
+    const uint32_t ki = sk[i];
+    const uint64_t ii = __ldcg(ws.inv + i);  // (in flight during the count)
+    const int64_t r = __ldcg(ws.row + i);
+    int cnt = 0;
+    unsigned tie = 0;
+#pragma unroll 8
+    for (int j = lane; j < mm; j += 32) {
+      const uint32_t kj = sk[j];
+      cnt += kj > ki;
+      tie |= kj == ki && j != i;
+    }
+    if (__any_sync(0xffffffffu, tie)) {
+      for (int j = lane; j < mm; j += 32) {
+        if (sk[j] != ki || j == i) continue;
+        const uint64_t ij = __ldcg(ws.inv + j);
+        cnt += ij > ii || (ij == ii && __ldcg(ws.row + j) < r);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0 && cnt < k_eff) {
+      out_ids[cnt] = id_of_inv(ii);
+      out_scores[cnt] = src.out_score(r, (uint64_t)ki);
+      if (out_rows) out_rows[cnt] = r;
+    }
+  }
+}
+
 // Phase D over a materialised score array (see header). Returns after writing the output.
 template <typename ST, typename Src>
 __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, const int64_t* ids,
