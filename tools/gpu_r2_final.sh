@@ -29,3 +29,5 @@ timeout 600 python tools/latency_probe.py c1 c3 c2 > gpurun_out/r2f_lat.log 2>&1
 timeout 900 python tools/ingest_bench.py 100000000 /tmp > gpurun_out/r2f_ingest.log 2>&1; tail -4 gpurun_out/r2f_ingest.log
 timeout 300 python tools/pq_score_probe.py > gpurun_out/r2f_pq_score.log 2>&1; OTF_PQ_SCORE_XOR=1 timeout 300 python tools/pq_score_probe.py >> gpurun_out/r2f_pq_score.log 2>&1; cat gpurun_out/r2f_pq_score.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:pq_score16 -s 3 -c 1 -o gpurun_out/prof_r2f_pq_score python tools/pq_score_probe.py > /dev/null 2>&1; echo full_pq_score=$?
+timeout 900 python tools/stress_cut.py 24 > gpurun_out/r2f_stress.log 2>&1; tail -3 gpurun_out/r2f_stress.log
+timeout 600 python tools/seg_probe.py 10000000 128 > gpurun_out/r2f_seg.log 2>&1; tail -1 gpurun_out/r2f_seg.log
