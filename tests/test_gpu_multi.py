@@ -202,15 +202,19 @@ def test_rank_many_sampled_threshold(otf, n, c, k):
     """Segments of >= 1M rows take the sampled-threshold selection (topk_seg_cut_kernel: a sample
     per classifier, one emission pass, rank by counting): lists equal the oracle's top_k of the
     scores, with a zero classifier (every row reaches T -> that segment's exact radix select), a
-    tie-heavy one, shuffled ids and unaligned segment starts; a following k beyond the plan (the
+    tie-heavy one, shuffled (and, for odd c, negative) ids and unaligned segment starts; a following k beyond the plan (the
     histogram path, same workspace) is unaffected."""
     rng = np.random.default_rng(n + c + k)
     x = np.round(rng.standard_normal((n, 64)) * 8).astype(np.float32) / 8
-    ids = rng.permutation(2 * n)[:n].astype(np.int64)
+    ids = rng.permutation(2 * n)[:n].astype(np.int64) - (n if c % 2 else 0)  # (negative ids: the signed tie order)
     W = rng.standard_normal((c, 64))
     W[0] = 0.0
     W[c // 2] = np.round(W[c // 2])
-    repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
+    if c % 2:  # a duck-typed store (FeatureStore itself rejects negative ids, as the reference's does)
+        store = type("Store", (), {"data": x, "ids": ids})()
+        repo = otf.Repository.dense(store)
+    else:
+        repo = otf.Repository.dense(otf.FeatureStore(x, ids=ids))
     S = repo.score_many(list(W))
     for kk in (k, 3000):
         lists = repo.rank_many([otf.LinearModel(w, 1, 1) for w in W], kk)
