@@ -1155,21 +1155,33 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
 #endif
 
   // ---- 3. selection ----------------------------------------------------------------------------
+  // the first kSelPre candidate keys are requested together with the count (one L2 round trip
+  // instead of two; keys past the count are stale and ignored)
+  constexpr int kSelPre = 4;
+  uint32_t kpre[kSelPre];
+#pragma unroll
+  for (int u = 0; u < kSelPre; ++u) kpre[u] = __ldcg(key32 + threadIdx.x + u * kCutScanThreads);
   const unsigned long long c_all = __ldcg(cut_count);
   const bool ok = usable && c_all >= (unsigned long long)k_eff && c_all <= (unsigned long long)kRcCand;
-  // the last CTA done with the shared counters clears them for the next query
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // the last CTA done with the shared counters clears them for the next query (on the fast path
+  // by the last warp after the keys are in place, off the ranking's critical path)
+  auto release_counters = [&]() {
     __threadfence();
     s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
     if (s_last) { ws.cut_word[0] = 0u; ws.cut_word[1] = 0u; ws.cut_word[8] = 0u; ws.cut_word[9] = 0u; ws.cut_word[6] = 0u; }
-  }
+  };
   if (ok) {
     uint32_t* sk = reinterpret_cast<uint32_t*>(sm);
     const int C = (int)c_all;
+#pragma unroll
+    for (int u = 0; u < kSelPre; ++u) {
+      const int t = threadIdx.x + u * kCutScanThreads;
+      if (t < C) sk[t] = kpre[u];
+    }
 #pragma unroll 4
-    for (int t = threadIdx.x; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
-    __syncthreads();
+    for (int t = threadIdx.x + kSelPre * kCutScanThreads; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
+    __syncthreads();  // (every thread of the CTA has read the count)
+    if (threadIdx.x == kCutScanThreads - 32) release_counters();
     // rank candidates i == vb (mod G): one warp per candidate counts who beats it
     for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
       const uint32_t ki = sk[q];
@@ -1211,6 +1223,8 @@ pq_rank_cut_kernel(const uint8_t* __restrict__ codes, int64_t n, const double* _
   }
   // ---- fallback: exact scores of every row, then the exact radix select -------------------------
   // (the LUT replica 0 in global memory is the float64 table the exact scores read)
+  __syncthreads();
+  if (threadIdx.x == 0) release_counters();
   __syncthreads();
   PqCutSrc src{PqBinSrc{nullptr, codes, lut_g, 16, K}};
   const int64_t nthreads = (int64_t)G * blockDim.x;
