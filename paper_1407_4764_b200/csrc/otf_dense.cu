@@ -412,11 +412,17 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
   DC_STAMP(4);
 
   // ---- 3. selection -------------------------------------------------------------------------------
+  // the first kSelPre x 256 candidate keys are requested together with the count (one L2 round
+  // trip instead of two; keys past the count are stale and ignored)
+  constexpr int kSelPre = 8;
+  uint32_t kpre[kSelPre];
+#pragma unroll
+  for (int u = 0; u < kSelPre; ++u) kpre[u] = __ldcg(key32 + threadIdx.x + u * kDcThreads);
   const unsigned long long c_all = __ldcg(cut_count);
   const bool ok = usable && c_all >= (unsigned long long)k_eff && c_all <= (unsigned long long)kDcSelCap;
-  // the last CTA done with the counters clears them for the next query
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // the last CTA done with the counters clears them for the next query (on the fast path by the
+  // last warp once the keys are in place, off the ranking's critical path)
+  auto release_counters = [&]() {
     __threadfence();
     s_last = atomicAdd(ws.cut_word + 6, 1u) == G - 1;
     if (s_last) {
@@ -426,13 +432,19 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
         ws.cut_word[kDcCtrWord + kDcCtrStride * q + 1] = 0u;
       }
     }
-  }
+  };
   if (ok) {
     uint32_t* sk = reinterpret_cast<uint32_t*>(dyn);
     const int C = (int)c_all;
+#pragma unroll
+    for (int u = 0; u < kSelPre; ++u) {
+      const int t = threadIdx.x + u * kDcThreads;
+      if (t < C) sk[t] = kpre[u];
+    }
 #pragma unroll 4
-    for (int t = threadIdx.x; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
-    __syncthreads();
+    for (int t = threadIdx.x + kSelPre * kDcThreads; t < C; t += blockDim.x) sk[t] = __ldcg(key32 + t);
+    __syncthreads();  // (every thread of the CTA has read the count)
+    if (threadIdx.x == kDcThreads - 32) release_counters();
     DC_STAMP(5);
     const int nw = blockDim.x >> 5;
     for (int q = (int)vb + wid * (int)G; q < C; q += nw * (int)G) {
@@ -472,6 +484,8 @@ dense_rank_cut(const float* __restrict__ X, int64_t n, const double* __restrict_
 #endif
     return;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) release_counters();
   if (usable) {  // the candidates cannot be used: every remaining row's score (static, interleaved)
     for (int64_t g = warp; g < ngroups; g += nwarp) {
       if (is_sample(g)) continue;  // warp-uniform
