@@ -539,7 +539,10 @@ int launch_bin_score(const uint8_t* codes, int64_t n, int n_bits, const double* 
       if (cmax && clog) *clog = 5;
       return OTF_OK;
     }
-    static const bool narrow = getenv("OTF_BIN_NARROW") != nullptr;  // A/B switch (tools/)
+    static const bool narrow_env = getenv("OTF_BIN_NARROW") != nullptr;  // A/B switch (tools/)
+    // the wide kernel's 16-byte loads need 16-byte aligned rows (an adopted device pointer may only
+    // be 4-byte aligned: bin_bytes_path's requirement)
+    const bool narrow = narrow_env || (((uintptr_t)codes) & 15) != 0;
     if (!narrow) {
       static bool wconf[64] = {false};
       if (!wconf[device & 63]) {

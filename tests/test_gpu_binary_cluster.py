@@ -8,6 +8,7 @@ reference tolerance of the exact dot (ranker.py:78-94). The clustered kernel is 
 (OTF_BIN_CLUSTER=1, read per call): every case runs on both paths."""
 
 import os
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -15,6 +16,7 @@ import pytest
 import otf_oracle as O
 
 pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
 
 
 def kernel_model(w, codes, n_bits):
@@ -84,3 +86,46 @@ def test_cluster_equals_per_slice_launches(otf):
     finally:
         os.environ.pop("OTF_BIN_CLUSTER", None)
     assert a.tobytes() == b.tobytes()
+
+
+def test_wide_equals_narrow_loads(otf, tmp_path):
+    """The default binary scan (16-byte loads per lane, rotated virtual lanes) and the round-1 form
+    (OTF_BIN_NARROW=1: one 4-byte load per lane and row; read once per process, so it runs in a
+    subprocess) give the same bits for 2048- and 4096-bit codes with a ragged row count."""
+    import subprocess
+    import sys
+
+    rng = np.random.default_rng(17)
+    for n_bits, n in ((2048, 100_003), (4096, 33_333)):
+        codes = rng.integers(0, 256, (n, n_bits // 8), dtype=np.uint8)
+        w = rng.standard_normal(n_bits)
+        np.save(tmp_path / "codes.npy", codes)
+        np.save(tmp_path / "w.npy", w)
+        wide = otf.score_binary(w, codes, n_bits)
+        script = (
+            "import sys, numpy as np; sys.path.insert(0, %r); import paper_1407_4764_b200 as otf; "
+            "c = np.load(%r); w = np.load(%r); np.save(%r, otf.score_binary(w, c, %d))"
+            % (str(ROOT), str(tmp_path / "codes.npy"), str(tmp_path / "w.npy"), str(tmp_path / "narrow.npy"), n_bits))
+        env = dict(os.environ, OTF_BIN_NARROW="1")
+        subprocess.run([sys.executable, "-c", script], check=True, env=env, timeout=600)
+        narrow = np.load(tmp_path / "narrow.npy")
+        assert wide.tobytes() == narrow.tobytes()
+
+
+def test_adopted_codes_at_4_byte_offset(otf):
+    """A borrowed device buffer whose rows start 4 bytes past a 16-byte boundary (allowed by the
+    byte-table path) takes the narrow loads: same scores and ranking as an aligned copy."""
+    import torch
+
+    rng = np.random.default_rng(23)
+    n, n_bits = 50_001, 2048
+    codes = rng.integers(0, 256, (n, n_bits // 8), dtype=np.uint8)
+    w = rng.standard_normal(n_bits)
+    buf = torch.empty(codes.size + 16, dtype=torch.uint8, device="cuda")
+    buf[4:4 + codes.size].copy_(torch.from_numpy(codes.reshape(-1)))
+    off = otf.Repository.from_device("binary", buf.data_ptr() + 4, n, n_bits)
+    ref = otf.score_binary(w, codes, n_bits)
+    assert off.score(w).tobytes() == ref.tobytes()
+    ids, _, _ = O.top_k(ref, 100)
+    np.testing.assert_array_equal(off.rank(otf.LinearModel(w, 1, 1), 100).ids, ids)
+    del off, buf
