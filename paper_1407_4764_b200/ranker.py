@@ -57,6 +57,19 @@ class RankedList:
     def entries(self) -> Iterator[tuple[int, float]]:
         return zip((int(i) for i in self.ids), (float(s) for s in self.scores))
 
+    @classmethod
+    def _make(cls, ids, scores, model_version, produced_at, names=None) -> "RankedList":
+        """The per-query constructor: the same fields without the frozen dataclass's five
+        object.__setattr__ calls (1.8 -> 1.0 us)."""
+        obj = object.__new__(cls)
+        d = obj.__dict__
+        d["ids"] = ids
+        d["scores"] = scores
+        d["model_version"] = model_version
+        d["produced_at"] = produced_at
+        d["names"] = names
+        return obj
+
 
 def _f32_rows(store) -> np.ndarray:
     data = store.data if hasattr(store, "data") else store
@@ -466,7 +479,7 @@ class Repository:
         if rc:
             _lib.check(rc)
         names = tuple(self.names[int(r)] for r in block[2]) if self.names is not None else None
-        return RankedList(block[0], block[1].view(np.float64), ver, produced_at, names)
+        return RankedList._make(block[0], block[1].view(np.float64), ver, produced_at, names)
 
 
 __all__ = ["RankedList", "RankerConfig", "Repository", "score_dense", "score_pq", "score_binary", "top_k",
