@@ -242,7 +242,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
       for (int b = threadIdx.x; b < kHistBinsMax; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
-    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+    rank_emit_any(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
     TOPK_STAMP(4);
     TOPK_REPORT();
     return;
@@ -296,7 +296,7 @@ topk_coop_kernel(Src src, int64_t n, const int64_t* __restrict__ ids, int64_t id
       for (int b = threadIdx.x; b < kHistBinsMax; b += blockDim.x) ws.hist[b] = 0u;
       if (threadIdx.x == 0) *ws.count = 0u;
     }
-    rank_emit(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+    rank_emit_any(src, ws, C, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
     TOPK_STAMP(4);
     TOPK_REPORT();
     return;

@@ -408,6 +408,17 @@ __device__ void rank_emit_k32(const Src& src, const TopkWs& ws, int64_t m, int64
   }
 }
 
+// Sources whose order keys fit in 32 bits (float32 scores): ranked with rank_emit_k32.
+template <typename Src> struct Key32 { static constexpr bool value = false; };
+template <> struct Key32<DirectSrc<float>> { static constexpr bool value = true; };
+template <typename Src>
+__device__ __forceinline__ void rank_emit_any(const Src& src, const TopkWs& ws, int64_t m, int64_t k_eff,
+                                              unsigned char* dyn, int64_t* out_ids, double* out_scores,
+                                              int64_t* out_rows, unsigned vb, unsigned vnb) {
+  if constexpr (Key32<Src>::value) rank_emit_k32(src, ws, m, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+  else rank_emit(src, ws, m, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+}
+
 // Phase D over a materialised score array (see header). Returns after writing the output.
 template <typename ST, typename Src>
 __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, const int64_t* ids,
@@ -493,7 +504,7 @@ __device__ void radix_select_emit(const ST* scores, const Src& src, int64_t n, c
   }
   if (k_eff <= kCandCap) {
     if (vb == 0 && threadIdx.x == 0) *ws.count = 0u;
-    rank_emit(src, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
+    rank_emit_any(src, ws, k_eff, k_eff, dyn, out_ids, out_scores, out_rows, vb, vnb);
     return;
   }
   // global bitonic sort over ws (capacity P)
